@@ -1,0 +1,163 @@
+/*
+ * mpfk.h -- C ABI of the B200-native DD/TD/QD GEMM (libmpfk.so).
+ *
+ * The reference (mpfkit, /root/reference/proj) exposes no C ABI: its drop-in
+ * surface is the header-only C++ template API in namespace mpfkit::linalg
+ * (SURVEY.md section 8(b)).  These entry points are exactly what a binding of
+ * that API to a GPU library needs; include/mpfk/linalg.hpp re-exposes them
+ * with the reference's C++ signatures, types and exceptions, and
+ * paper_2101_06584_b200/__init__.py binds them with ctypes.  Each function
+ * cites the reference interface it replaces (paths relative to
+ * /root/reference/proj).
+ *
+ * Conventions
+ *  - A width-W matrix is W component planes (component 0 leads), each a
+ *    row-major rows x stride binary64 array; plane w starts at
+ *    base + w * plane_stride.  This is MPMatrix<W>'s layout
+ *    (include/mpfkit/linalg.hpp:36-129, pad_columns :32-34) when
+ *    stride == pad4(cols) and plane_stride == rows * stride.
+ *  - Every call returns MPFK_OK or an error code; the message (identical to
+ *    the reference's exception text where one exists) is in
+ *    mpfk_last_error(), which is thread-local.
+ *  - Results are bit-identical to the reference's per-element accumulation
+ *    order (linalg.hpp:338-344) for every variant, n_min and GPU count.
+ *  - There is no CPU fallback: without a usable GPU every compute call fails
+ *    with MPFK_ENODEV.
+ */
+#ifndef MPFK_H_
+#define MPFK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPFK_ABI_VERSION 1
+
+/* error codes; the C++ shim maps them to the reference's exception types */
+enum mpfk_status {
+  MPFK_OK = 0,
+  MPFK_EINVAL = 1,   /* std::invalid_argument (linalg.hpp:283-293, :409; config.hpp:25-28) */
+  MPFK_ERUNTIME = 2, /* std::runtime_error (runtime.cpp:73-80: FP environment) */
+  MPFK_ECUDA = 3,    /* CUDA runtime failure (message carries cudaGetErrorString) */
+  MPFK_ENOMEM = 4,   /* std::bad_alloc (linalg.hpp:116) */
+  MPFK_ENODEV = 5    /* no usable sm_100 device: there is no CPU fallback */
+};
+
+/* KernelVariant, linalg.hpp:149.  All three are bit-identical on the GPU
+ * (one kernel); the value is validated exactly like the reference
+ * (SIMD variants need n_min % 4 == 0, linalg.hpp:290-294). */
+enum mpfk_variant { MPFK_NORMAL = 0, MPFK_SIMD_SET = 1, MPFK_SIMD_LOADSTORE = 2 };
+
+typedef struct mpfk_mat {
+  double *base;          /* W planes */
+  uint64_t rows, cols;
+  uint64_t stride;       /* row stride in doubles, >= cols */
+  uint64_t plane_stride; /* doubles between planes; 0 means rows * stride */
+} mpfk_mat;
+
+/* Timings of the last host-buffer GEMM on this thread (device clocks, ms). */
+typedef struct mpfk_stats {
+  double h2d_ms;    /* host->device copies of A shards and B slices */
+  double bcast_ms;  /* B replication over NVLink (peer all-gather), G > 1 */
+  double kernel_ms; /* max over GPUs of the GEMM kernel */
+  double d2h_ms;    /* device->host copy of the C shards */
+  double total_ms;  /* whole call, host wall clock */
+  uint64_t h2d_bytes, d2h_bytes, peer_bytes;
+  int n_gpus;
+  int kernel_launches;
+} mpfk_stats;
+
+/* ---- runtime (runtime.hpp:10-30, runtime.cpp:48-81) -------------------- */
+
+/* Once-init of the device context(s): checks for sm_100 devices and runs the
+ * device FP-environment self-test (the twin of verify_fp_environment,
+ * runtime.cpp:19-38,72-81) on each.  n_gpus <= 0 means all visible devices.
+ * Idempotent; compute calls initialise lazily. */
+int mpfk_init(int n_gpus);
+void mpfk_shutdown(void);
+const char *mpfk_last_error(void);
+int mpfk_abi_version(void);
+/* number of usable devices (0 when none); never fails */
+int mpfk_device_count(void);
+/* Device self-test on the current device: binary64 round-to-nearest-even and
+ * a correctly rounded fused multiply-add (runtime.cpp:19-38). */
+int mpfk_selftest(void);
+
+/* ---- GEMM, host buffers: the drop-in for linalg::matmul_*_into --------- */
+
+/* matmul_block_parallel_into(C, A, B, n_min, variant, workers),
+ * linalg.hpp:402-433.  Validates shapes and n_min before any device work
+ * with the reference's messages; clears C (fill_zero, linalg.hpp:94-96),
+ * computes C = A*B on min(workers, devices) GPUs sharding C by contiguous
+ * row spans (the reference's worker partition, linalg.hpp:413-421), leaves
+ * C's padding cells +0 (zero_pads, :99-106) and bumps the op counters
+ * (count_matmul, :175-180).  Synchronous: returns once C is on the host.
+ * workers: 1..; GPUs actually used = min(workers, device count, row blocks). */
+int mpfk_matmul_block_parallel_into(int width, mpfk_mat *C, const mpfk_mat *A, const mpfk_mat *B,
+                                    uint64_t n_min, int variant, unsigned workers);
+/* matmul_block_into, linalg.hpp:368-388 (one GPU) */
+int mpfk_matmul_block_into(int width, mpfk_mat *C, const mpfk_mat *A, const mpfk_mat *B,
+                           uint64_t n_min, int variant);
+/* matmul_naive_into, linalg.hpp:346-358 (same result by construction) */
+int mpfk_matmul_naive_into(int width, mpfk_mat *C, const mpfk_mat *A, const mpfk_mat *B,
+                           int variant);
+int mpfk_last_stats(mpfk_stats *out);
+
+/* ---- GEMM, device-resident operands ------------------------------------ */
+
+/* C[0:m,0:n] = A[0:m,0:k] * B[0:k,0:n] on the CURRENT device, enqueued on
+ * `stream` (a cudaStream_t; NULL = legacy default stream), asynchronous.
+ * Pointers are device memory of that device, 16-byte aligned, with even row
+ * strides (pad4 strides of the reference layout qualify).  Only the m x n
+ * cells of C are written.  k == 0 writes +0 into C.  Counts ops like
+ * count_matmul.  Returns the number of kernel launches through *launches
+ * when non-NULL. */
+int mpfk_gemm_device(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                     uint64_t lda, uint64_t a_plane, const double *B, uint64_t ldb,
+                     uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, void *stream,
+                     int *launches);
+
+/* ---- elementwise width kernels (mpf::add/mul<W>, mpf.hpp:341-353) ------- */
+
+/* r[i] = op(x[i], y[i]) for `count` values stored AoS (W doubles each) in
+ * host memory, computed on the GPU.  op: 0 = add, 1 = mul (library
+ * defaults for the width, mpf.hpp:242-260).  Used by the arithmetic parity
+ * sweeps. */
+int mpfk_binop_batch(int width, int op, uint64_t count, const double *x, const double *y,
+                     double *r);
+
+/* ---- op counters (linalg.hpp:160-180, linalg.cpp:10-25) ----------------- */
+void mpfk_op_counters_reset(void);
+void mpfk_op_counters_read(uint64_t *adds, uint64_t *muls, uint64_t *leaf_multiplies);
+
+/* ---- pinned host memory for MPMatrix-style buffers ----------------------- */
+/* aligned (>= 256 B), page-locked: host<->device copies run at full PCIe
+ * bandwidth.  Replaces aligned_alloc(32, .) of linalg.hpp:115. */
+void *mpfk_host_alloc(uint64_t bytes);
+void mpfk_host_free(void *p);
+
+/* ---- seeded inputs (random.hpp:17-75) --------------------- */
+/* The BASELINE.json configurations, generated row-parallel on the host:
+ * per-row SplitMix64 stream state = seed ^ ((row+1) * 0xd1b54a32d192ed03);
+ * narrow (wide == 0): c0 = 2u - 1; wide: c0 = +-(1+u) * 2^(x mod 61 - 30);
+ * c_{i+1} = c_i * 2^-53 * (2u - 1); W == 2 -> quick_two_sum, W > 2 ->
+ * renormalized<W> (mpf.hpp:76-88).  Pads (stride - cols) are set to +0.
+ * Rows [row0, row0 + rows) of the seeded matrix are written (a row shard).
+ * threads <= 0: hardware concurrency. */
+int mpfk_fill_baseline(int width, int wide, uint64_t row0, uint64_t rows, uint64_t cols,
+                       uint64_t stride, uint64_t seed, double *planes, int threads);
+
+/* FP64 pipe microbenchmark on the current device: returns measured FP64
+ * lane-operations per second (each DADD/DMUL/DFMA counted once), the
+ * denominator of the roofline fraction (MEASURED_PEAKS.json has no FP64
+ * entry). */
+int mpfk_fp64_peak(double *ops_per_s, double *ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPFK_H_ */

@@ -1,0 +1,173 @@
+"""Test-infrastructure checkers (never the product path).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
+import this package.
+
+  orc   -- ctypes binding of _build/libmpfk_oracle.so, the C restatement of the
+           reference's GEMM path (mpfk_oracle.c)
+  ref   -- ctypes binding of _ref/libmpfkref.so, the UNMODIFIED reference
+           (mpfkit) compiled here from /root/reference/proj by oracle/Makefile
+  dyadic -- exact dyadic-rational arithmetic (the reference's DyadicReal
+           semantics, proj/src/oracle.cpp) for error-bound checks
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libmpfk_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libmpfkref.so")
+
+_D = C.c_void_p
+_S = C.c_size_t
+_U64 = C.c_uint64
+
+_orc = None
+_ref = None
+
+
+def _p(a):
+    return a.ctypes.data
+
+
+def orc():
+    global _orc
+    if _orc is None:
+        L = C.CDLL(ORACLE_SO)
+        L.orc_gemm.argtypes = [C.c_int, _S, _S, _S, _D, _S, _D, _S, _D, _S]
+        L.orc_gemm_rows.argtypes = [C.c_int, _S, _S, _S, _D, _S, _D, _S, _D, _S, _S, _S]
+        L.orc_add.argtypes = [C.c_int, _D, _D, _D]
+        L.orc_mul.argtypes = [C.c_int, _D, _D, _D]
+        L.orc_renorm5.argtypes = [_D, _D]
+        L.orc_vseb.argtypes = [_D, _S, _D, _S]
+        L.orc_vec_sum.argtypes = [_D, _S, _D]
+        L.orc_two_sum.argtypes = [C.c_double, C.c_double, _D, _D]
+        L.orc_quick_two_sum.argtypes = [C.c_double, C.c_double, _D, _D]
+        L.orc_two_prod.argtypes = [C.c_double, C.c_double, _D, _D]
+        L.orc_fill_random.argtypes = [C.c_int, _S, _S, _S, _U64, _D]
+        L.orc_fill_baseline.argtypes = [C.c_int, C.c_int, _S, _S, _S, _S, _U64, _D]
+        L.orc_gen_paper.argtypes = [C.c_int, _S, _S, _D, _D]
+        L.orc_random_normalized.argtypes = [C.c_int, _D, _D]
+        L.orc_sm64_next.argtypes = [_D]
+        L.orc_sm64_next.restype = _U64
+        _orc = L
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        L = C.CDLL(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_gemm.argtypes = [C.c_int, _S, _S, _S, _D, _S, _D, _S, _D, _S, _S, C.c_int, C.c_uint, C.c_int,
+                               C.c_int, C.c_int]
+        L.ref_gemm_shapes.argtypes = [C.c_int, _S, _S, _S, _S, _S, _S, _S, C.c_int, C.c_uint]
+        L.ref_fill_random.argtypes = [C.c_int, _S, _S, _U64, _D, _S]
+        L.ref_gen_paper.argtypes = [C.c_int, _S, _D, _D, _S]
+        L.ref_binop.argtypes = [C.c_int, C.c_int, _D, _D, _D]
+        L.ref_binop_batch.argtypes = [C.c_int, C.c_int, _S, _D, _D, _D]
+        L.ref_renorm5.argtypes = [_D, _D]
+        L.ref_vseb.argtypes = [_D, _S, _D, _S]
+        L.ref_two_sum.argtypes = [C.c_double, C.c_double, _D, _D]
+        L.ref_quick_two_sum.argtypes = [C.c_double, C.c_double, _D, _D]
+        L.ref_two_prod.argtypes = [C.c_double, C.c_double, _D, _D]
+        L.ref_op_counts.argtypes = [_D, _D]
+        L.ref_random_normalized.argtypes = [C.c_int, _D, C.c_int, _D]
+        L.ref_hardware_concurrency.restype = C.c_uint
+        _ref = L
+    return _ref
+
+
+# ---- convenience wrappers over (W, rows, ld) float64 plane arrays ------------
+
+def planes(W, rows, cols, ld=None):
+    ld = ld if ld is not None else (cols + 3) & ~3
+    return np.zeros((W, rows, ld), dtype=np.float64)
+
+
+def orc_gemm(A: np.ndarray, B: np.ndarray, K: int, n: int, rows=None) -> np.ndarray:
+    """Oracle C = A*B over padded plane arrays (W, m, lda), (W, K, ldb)."""
+    W, m, lda = A.shape
+    ldb = B.shape[2]
+    ldc = (n + 3) & ~3
+    Cm = np.zeros((W, m, ldc), dtype=np.float64)
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    r0, r1 = (0, m) if rows is None else rows
+    orc().orc_gemm_rows(W, m, K, n, _p(A), lda, _p(B), ldb, _p(Cm), ldc, r0, r1)
+    return Cm
+
+
+def ref_gemm(A: np.ndarray, B: np.ndarray, K: int, n: int, workers=None, n_min=32, variant=2,
+             naive=False) -> np.ndarray:
+    """The reference's matmul_block_parallel_into on plane arrays."""
+    W, m, lda = A.shape
+    ldb = B.shape[2]
+    ldc = (n + 3) & ~3
+    Cm = np.zeros((W, m, ldc), dtype=np.float64)
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    if workers is None:
+        workers = max(1, os.cpu_count() or 1)
+    rc = ref().ref_gemm(W, m, K, n, _p(A), lda, _p(B), ldb, _p(Cm), ldc, n_min, variant, workers,
+                        int(naive), -1, -1)
+    if rc:
+        raise ValueError(ref().ref_last_error().decode())
+    return Cm
+
+
+def ref_fill_random(W, rows, cols, seed):
+    a = planes(W, rows, cols)
+    ref().ref_fill_random(W, rows, cols, seed, _p(a), a.shape[2])
+    return a
+
+
+def orc_fill_random(W, rows, cols, seed):
+    a = planes(W, rows, cols)
+    orc().orc_fill_random(W, rows, cols, a.shape[2], seed, _p(a))
+    return a
+
+
+def orc_fill_baseline(W, rows, cols, seed, wide=False, row0=0):
+    a = planes(W, rows, cols)
+    orc().orc_fill_baseline(W, int(wide), row0, rows, cols, a.shape[2], seed, _p(a))
+    return a
+
+
+def ref_gen_paper(W, n):
+    A = planes(W, n, n)
+    B = planes(W, n, n)
+    ref().ref_gen_paper(W, n, _p(A), _p(B), A.shape[2])
+    return A, B
+
+
+def orc_gen_paper(W, n):
+    A = planes(W, n, n)
+    B = planes(W, n, n)
+    orc().orc_gen_paper(W, n, A.shape[2], _p(A), _p(B))
+    return A, B
+
+
+def ref_binop_batch(W, op, x, y):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    r = np.empty_like(x)
+    ref().ref_binop_batch(W, {"add": 0, "mul": 1}[op], x.shape[0], _p(x), _p(y), _p(r))
+    return r
+
+
+def orc_binop_batch(W, op, x, y):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    r = np.empty_like(x)
+    f = orc().orc_add if op == "add" else orc().orc_mul
+    for i in range(x.shape[0]):
+        f(W, x[i].ctypes.data, y[i].ctypes.data, r[i].ctypes.data)
+    return r

@@ -1,0 +1,244 @@
+// ref_driver.cpp -- a C-ABI shim over the UNMODIFIED reference (mpfkit).
+//
+// TEST INFRASTRUCTURE ONLY (the checker and the reported CPU baseline; never
+// the shipped path).  Compiled by oracle/build_ref.sh together with the
+// reference's own proj/src/runtime.cpp and proj/src/linalg.cpp, straight from
+// where they lie under /root/reference, into oracle/_ref/libmpfkref.so.  No
+// reference source is copied into this repository.
+//
+// Every entry point only marshals plain SoA arrays into mpfkit types and
+// calls the reference's public API:
+//   ref_gemm        -> mpfkit::linalg::matmul_block_parallel_into (linalg.hpp:402-433)
+//   ref_gemm_naive  -> mpfkit::linalg::matmul_naive_into          (linalg.hpp:346-358)
+//   ref_add/ref_mul -> mpfkit::mpf::add/mul<W>                    (mpf.hpp:341-353)
+//   ref_fill_random -> the loop of bench::fill_random (bench.cpp:295-302) over
+//                      rng::random_normalized<W> (random.hpp:54-67); bench.cpp
+//                      itself needs Boost, which this image lacks
+//   ref_gen_paper   -> the loop of bench::gen_paper_matrices (bench.cpp:278-292)
+//   ref_renorm5 / ref_vseb / ref_two_* -> mpfkit::eft (eft.hpp)
+//   ref_op_counts   -> linalg::op_counters_read (linalg.cpp:13-25)
+// Errors: reference exceptions become a nonzero return and a message in
+// ref_last_error().
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+
+#include "mpfkit/linalg.hpp"
+#include "mpfkit/random.hpp"
+#include "mpfkit/runtime.hpp"
+
+using namespace mpfkit;
+
+namespace {
+thread_local std::string g_err;
+
+template <int W>
+linalg::MPMatrix<W> load(const double* planes, std::size_t rows, std::size_t cols,
+                         std::size_t ld) {
+  linalg::MPMatrix<W> m(rows, cols);
+  const std::size_t ps = rows * ld;
+  for (int w = 0; w < W; ++w)
+    for (std::size_t i = 0; i < rows; ++i)
+      std::memcpy(m.plane(w) + i * m.stride(), planes + w * ps + i * ld,
+                  cols * sizeof(double));
+  return m;
+}
+
+template <int W>
+void store(const linalg::MPMatrix<W>& m, double* planes, std::size_t ld) {
+  const std::size_t ps = m.rows() * ld;
+  for (int w = 0; w < W; ++w)
+    for (std::size_t i = 0; i < m.rows(); ++i)
+      std::memcpy(planes + w * ps + i * ld, m.plane(w) + i * m.stride(),
+                  m.cols() * sizeof(double));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+template <int W>
+int gemm_w(std::size_t m, std::size_t K, std::size_t n, const double* A, std::size_t lda,
+           const double* B, std::size_t ldb, double* C, std::size_t ldc, std::size_t n_min,
+           int variant, unsigned workers, int naive, int c_rows, int c_cols) {
+  return guarded([&] {
+    const auto a = load<W>(A, m, K, lda);
+    const auto b = load<W>(B, K, n, ldb);
+    linalg::MPMatrix<W> c(c_rows < 0 ? m : static_cast<std::size_t>(c_rows),
+                          c_cols < 0 ? n : static_cast<std::size_t>(c_cols));
+    const auto v = static_cast<linalg::KernelVariant>(variant);
+    if (naive)
+      linalg::matmul_naive_into(c, a, b, v);
+    else
+      linalg::matmul_block_parallel_into(c, a, b, n_min, v, workers);
+    store<W>(c, C, ldc);
+  });
+}
+
+template <int W>
+void fill_random_w(std::size_t rows, std::size_t cols, std::uint64_t seed, double* planes,
+                   std::size_t ld) {
+  rng::SplitMix64 g(seed);
+  std::memset(planes, 0, sizeof(double) * W * rows * ld);
+  for (std::size_t i = 0; i < rows; ++i)
+    for (std::size_t j = 0; j < cols; ++j) {
+      const auto v = rng::random_normalized<W>(g);
+      for (int w = 0; w < W; ++w) planes[w * rows * ld + i * ld + j] = v.c[w];
+    }
+}
+
+template <int W>
+void gen_paper_w(std::size_t n, double* A, double* B, std::size_t ld) {
+  std::memset(A, 0, sizeof(double) * W * n * ld);
+  std::memset(B, 0, sizeof(double) * W * n * ld);
+  const auto r5 = mpf::from_f64<W>(std::sqrt(5.0));
+  const auto r3 = mpf::from_f64<W>(std::sqrt(3.0));
+  for (std::size_t i = 1; i <= n; ++i) {
+    const auto brow = mpf::mul(r3, mpf::from_f64<W>(static_cast<double>(n - i)));
+    for (std::size_t j = 1; j <= n; ++j) {
+      const auto a = mpf::mul(r5, mpf::from_f64<W>(static_cast<double>(i + j - 1)));
+      for (int w = 0; w < W; ++w) {
+        A[w * n * ld + (i - 1) * ld + (j - 1)] = a.c[w];
+        B[w * n * ld + (i - 1) * ld + (j - 1)] = brow.c[w];
+      }
+    }
+  }
+}
+
+template <int W>
+void binop_w(int op, const double* x, const double* y, double* r) {
+  mpf::MultiDouble<W> a, b;
+  for (int w = 0; w < W; ++w) a.c[w] = x[w], b.c[w] = y[w];
+  const auto c = op == 0 ? mpf::add(a, b) : mpf::mul(a, b);
+  for (int w = 0; w < W; ++w) r[w] = c.c[w];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+unsigned ref_hardware_concurrency(void) { return std::thread::hardware_concurrency(); }
+
+// 1 when the reference picked its AVX2 backend (runtime.cpp:48-57).
+int ref_backend_is_hardware(void) {
+  return runtime::active_backend() == runtime::Backend::hardware ? 1 : 0;
+}
+
+// variant: 0 NORMAL, 1 SIMD_SET, 2 SIMD_LOADSTORE (linalg.hpp:149).
+// c_rows/c_cols < 0 -> C is m x n; otherwise a deliberately mis-shaped C
+// (exercises "matmul: result shape mismatch").
+int ref_gemm(int W, std::size_t m, std::size_t K, std::size_t n, const double* A,
+             std::size_t lda, const double* B, std::size_t ldb, double* C, std::size_t ldc,
+             std::size_t n_min, int variant, unsigned workers, int naive, int c_rows,
+             int c_cols) {
+  switch (W) {
+    case 2: return gemm_w<2>(m, K, n, A, lda, B, ldb, C, ldc, n_min, variant, workers, naive, c_rows, c_cols);
+    case 3: return gemm_w<3>(m, K, n, A, lda, B, ldb, C, ldc, n_min, variant, workers, naive, c_rows, c_cols);
+    case 4: return gemm_w<4>(m, K, n, A, lda, B, ldb, C, ldc, n_min, variant, workers, naive, c_rows, c_cols);
+  }
+  g_err = "bad width";
+  return 1;
+}
+
+// Shape-check probe with arbitrary (mismatched) A/B/C shapes; no data.
+int ref_gemm_shapes(int W, std::size_t am, std::size_t ak, std::size_t bk, std::size_t bn,
+                    std::size_t cm, std::size_t cn, std::size_t n_min, int variant,
+                    unsigned workers) {
+  return guarded([&] {
+    if (W != 2) throw std::invalid_argument("probe is DD only");
+    linalg::MPMatrix<2> a(am, ak), b(bk, bn), c(cm, cn);
+    linalg::matmul_block_parallel_into(c, a, b, n_min,
+                                       static_cast<linalg::KernelVariant>(variant), workers);
+  });
+}
+
+void ref_op_counters_reset(void) { linalg::op_counters_reset(); }
+void ref_op_counts(std::uint64_t* adds, std::uint64_t* muls) {
+  const auto c = linalg::op_counters_read();
+  *adds = c.adds, *muls = c.muls;
+}
+
+int ref_fill_random(int W, std::size_t rows, std::size_t cols, std::uint64_t seed,
+                    double* planes, std::size_t ld) {
+  if (W == 2) fill_random_w<2>(rows, cols, seed, planes, ld);
+  else if (W == 3) fill_random_w<3>(rows, cols, seed, planes, ld);
+  else if (W == 4) fill_random_w<4>(rows, cols, seed, planes, ld);
+  else return 1;
+  return 0;
+}
+
+int ref_gen_paper(int W, std::size_t n, double* A, double* B, std::size_t ld) {
+  if (W == 2) gen_paper_w<2>(n, A, B, ld);
+  else if (W == 3) gen_paper_w<3>(n, A, B, ld);
+  else if (W == 4) gen_paper_w<4>(n, A, B, ld);
+  else return 1;
+  return 0;
+}
+
+// op: 0 add (library default for the width), 1 mul
+int ref_binop(int W, int op, const double* x, const double* y, double* r) {
+  if (W == 2) binop_w<2>(op, x, y, r);
+  else if (W == 3) binop_w<3>(op, x, y, r);
+  else if (W == 4) binop_w<4>(op, x, y, r);
+  else return 1;
+  return 0;
+}
+
+// Batched forms for million-sample sweeps (one call, no per-call overhead).
+int ref_binop_batch(int W, int op, std::size_t count, const double* x, const double* y,
+                    double* r) {
+  for (std::size_t i = 0; i < count; ++i)
+    if (ref_binop(W, op, x + i * W, y + i * W, r + i * W)) return 1;
+  return 0;
+}
+
+void ref_renorm5(const double* c, double* r) {
+  const auto o = eft::renorm5(c[0], c[1], c[2], c[3], c[4]);
+  for (int i = 0; i < 4; ++i) r[i] = o[i];
+}
+
+int ref_vseb(const double* e, std::size_t n, double* out, std::size_t k) {
+  return guarded([&] { eft::vseb(std::span<const double>(e, n), std::span<double>(out, k)); });
+}
+
+void ref_two_sum(double a, double b, double* s, double* e) {
+  const auto p = eft::two_sum(a, b);
+  *s = p.s, *e = p.e;
+}
+void ref_quick_two_sum(double a, double b, double* s, double* e) {
+  const auto p = eft::ScalarEft::quick_two_sum(a, b);
+  *s = p.s, *e = p.e;
+}
+void ref_two_prod(double a, double b, double* s, double* e) {
+  const auto p = eft::two_prod(a, b);
+  *s = p.s, *e = p.e;
+}
+
+void ref_random_normalized(int W, std::uint64_t* state, int is_signed, double* out) {
+  rng::SplitMix64 g(0);
+  g.state = *state;
+  if (W == 2) {
+    const auto v = is_signed ? rng::random_normalized_signed<2>(g) : rng::random_normalized<2>(g);
+    for (int w = 0; w < 2; ++w) out[w] = v.c[w];
+  } else if (W == 3) {
+    const auto v = is_signed ? rng::random_normalized_signed<3>(g) : rng::random_normalized<3>(g);
+    for (int w = 0; w < 3; ++w) out[w] = v.c[w];
+  } else {
+    const auto v = is_signed ? rng::random_normalized_signed<4>(g) : rng::random_normalized<4>(g);
+    for (int w = 0; w < 4; ++w) out[w] = v.c[w];
+  }
+  *state = g.state;
+}
+
+}  // extern "C"

@@ -1,0 +1,802 @@
+// capi.cu -- host runtime and C ABI of libmpfk.so (declared in include/mpfk.h).
+//
+// Replaces the reference's runtime + GEMM drivers:
+//   runtime::verify_fp_environment / active_backend  (runtime.cpp:19-81)
+//     -> per-device context with a device FP self-test, lazily initialised
+//   linalg::matmul_{naive,block,block_parallel}_into (linalg.hpp:346-433)
+//     -> shape/n_min validation with the reference's messages, then the
+//        sm_100a GEMM kernel on 1..G GPUs with C sharded by row spans
+//   run_on_threads (linalg.hpp:314-334) -> one host thread per GPU
+//   count_matmul / op counters (linalg.hpp:160-180, linalg.cpp:10-25)
+//   rng + fill generators (random.hpp)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/mpfk.h"
+#include "gemm_kernel.cuh"
+#include "mpf_arith.cuh"
+
+namespace {
+
+using namespace mpfk;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+thread_local std::string t_err;
+thread_local mpfk_stats t_stats{};
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear sticky-free errors
+    fail(MPFK_ECUDA, std::string("mpfk: ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MPFK_OK;
+  } catch (const Fail& e) {
+    t_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    t_err = "std::bad_alloc";
+    return MPFK_ENOMEM;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return MPFK_ERUNTIME;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// op counters, linalg.cpp:10-25 / count_matmul linalg.hpp:175-180
+// ---------------------------------------------------------------------------
+std::atomic<uint64_t> g_adds{0}, g_muls{0}, g_leaf{0};
+
+void count_matmul(uint64_t m, uint64_t n, uint64_t k) {
+  if (k == 0) return;
+  g_muls.fetch_add(m * n * k, std::memory_order_relaxed);
+  g_adds.fetch_add(m * n * (k - 1), std::memory_order_relaxed);
+}
+
+// ---------------------------------------------------------------------------
+// device self-test, the twin of runtime.cpp:19-38.  Operands come from
+// global memory so nothing is constant-folded by the compiler.
+// ---------------------------------------------------------------------------
+__global__ void selftest_kernel(const double* in, int* ok) {
+  const double one = in[0], tiny = in[1], three_half = in[2], big = in[3], c = in[4];
+  bool r = true;
+  r &= __dadd_rn(one, tiny) == 1.0;                     // tie -> even
+  r &= __dsub_rn(-one, tiny) == -1.0;
+  r &= __dadd_rn(one, three_half) == 1.0 + 0x1p-52;     // above the tie rounds away
+  r &= __dsub_rn(-one, three_half) == -1.0 - 0x1p-52;
+  const bool rn = r;
+  const bool fused = __fma_rn(big, big, c) == 1.0;      // (2^27+1)^2 - (2^54+2^28)
+  *ok = (rn ? 1 : 0) | (fused ? 2 : 0);
+}
+
+struct Device {
+  int id = -1;
+  bool ready = false;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  // grow-only operand buffers for the host-buffer path
+  double* dA = nullptr;
+  double* dB = nullptr;
+  double* dC = nullptr;
+  size_t capA = 0, capB = 0, capC = 0;
+};
+
+std::mutex g_mu;
+std::vector<Device> g_dev;
+int g_ndev = -1;
+
+int visible_sm100_devices() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int usable = 0;
+  for (int d = 0; d < n; ++d) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, d) != cudaSuccess) continue;
+    if (p.major == 10 && p.minor == 0) ++usable;
+  }
+  return usable == n ? n : usable;
+}
+
+void run_selftest_current() {
+  const double h_in[5] = {1.0, 0x1p-53, 0x1.8p-53, 0x1p27 + 1.0, -(0x1p54 + 0x1p28)};
+  double* d_in = nullptr;
+  int* d_ok = nullptr;
+  ck(cudaMalloc(&d_in, sizeof h_in), "cudaMalloc(selftest)");
+  ck(cudaMalloc(&d_ok, sizeof(int)), "cudaMalloc(selftest)");
+  ck(cudaMemcpy(d_in, h_in, sizeof h_in, cudaMemcpyHostToDevice), "selftest H2D");
+  selftest_kernel<<<1, 1>>>(d_in, d_ok);
+  ck(cudaGetLastError(), "selftest launch");
+  int ok = 0;
+  ck(cudaMemcpy(&ok, d_ok, sizeof ok, cudaMemcpyDeviceToHost), "selftest D2H");
+  cudaFree(d_in);
+  cudaFree(d_ok);
+  if (!(ok & 1))
+    fail(MPFK_ERUNTIME,
+         "mpfk: binary64 arithmetic is not rounding to nearest-even; "
+         "the extended-precision kernels are unusable in this environment");
+  if (!(ok & 2))
+    fail(MPFK_ERUNTIME,
+         "mpfk: fma is not a correctly rounded fused multiply-add; "
+         "the extended-precision kernels are unusable in this environment");
+}
+
+// Lazily initialise devices [0, n).  Caller holds no lock.
+void ensure_devices(int n) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_ndev < 0) {
+    g_ndev = visible_sm100_devices();
+    g_dev.resize(std::max(g_ndev, 0));
+    for (int d = 0; d < g_ndev; ++d) g_dev[d].id = d;
+  }
+  if (g_ndev == 0)
+    fail(MPFK_ENODEV,
+         "mpfk: no CUDA sm_100 device is visible; the GPU library has no CPU fallback");
+  if (n > g_ndev) n = g_ndev;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (int d = 0; d < n; ++d) {
+    Device& D = g_dev[d];
+    if (D.ready) continue;
+    ck(cudaSetDevice(d), "cudaSetDevice");
+    run_selftest_current();
+    ck(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : D.ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    D.ready = true;
+  }
+  cudaSetDevice(prev);
+}
+
+void grow(double*& p, size_t& cap, size_t bytes) {
+  if (bytes <= cap) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  ck(cudaMalloc(&p, bytes), "cudaMalloc(operand buffer)");
+  cap = bytes;
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch per width
+// ---------------------------------------------------------------------------
+using Cfg2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 2>;
+using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1>;
+using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1>;
+
+template <class Cfg>
+void launch_cfg(const kern::GemmArgs& g, cudaStream_t s) {
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    ck(cudaFuncSetAttribute(kern::mpgemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)Cfg::SMEM),
+       "cudaFuncSetAttribute");
+    configured_dev = dev;
+  }
+  dim3 grid((g.N + Cfg::BN - 1) / Cfg::BN, (g.M + Cfg::BM - 1) / Cfg::BM);
+  kern::mpgemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g);
+  ck(cudaGetLastError(), "GEMM kernel launch");
+}
+
+__global__ void zero_planes_kernel(double* C, long long ldc, long long pc, int M, int N, int W) {
+  const long long total = (long long)W * M * N;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int w = (int)(t / ((long long)M * N));
+    const long long r = t % ((long long)M * N);
+    C[w * pc + (r / N) * ldc + (r % N)] = 0.0;
+  }
+}
+
+// Enqueue C = A*B on the current device.  Returns kernel launches.
+int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                 uint64_t pa, const double* B, uint64_t ldb, uint64_t pb, double* C,
+                 uint64_t ldc, uint64_t pc, cudaStream_t s) {
+  if (m == 0 || n == 0) return 0;
+  if (m > 0x7fffffffULL || n > 0x7fffffffULL || k > 0x7fffffffULL)
+    fail(MPFK_EINVAL, "mpfk: dimension exceeds 2^31-1");
+  if (k == 0) {
+    zero_planes_kernel<<<std::min<uint64_t>((W * m * n + 255) / 256, 4096), 256, 0, s>>>(
+        C, (long long)ldc, (long long)pc, (int)m, (int)n, W);
+    ck(cudaGetLastError(), "zero kernel launch");
+    return 1;
+  }
+  kern::GemmArgs g;
+  g.A = A, g.B = B, g.C = C;
+  g.lda = (long long)lda, g.ldb = (long long)ldb, g.ldc = (long long)ldc;
+  g.pa = (long long)pa, g.pb = (long long)pb, g.pc = (long long)pc;
+  g.M = (int)m, g.N = (int)n, g.K = (int)k;
+  switch (W) {
+    case 2: launch_cfg<Cfg2>(g, s); break;
+    case 3: launch_cfg<Cfg3>(g, s); break;
+    case 4: launch_cfg<Cfg4>(g, s); break;
+    default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
+  }
+  return 1;
+}
+
+void check_width(int W) {
+  if (W < 2 || W > 4) fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
+}
+
+uint64_t plane_of(const mpfk_mat* M) {
+  return M->plane_stride ? M->plane_stride : M->rows * M->stride;
+}
+
+void check_mat(const mpfk_mat* M, const char* name) {
+  if (!M) fail(MPFK_EINVAL, std::string("mpfk: null matrix ") + name);
+  if (M->stride < M->cols) fail(MPFK_EINVAL, std::string("mpfk: stride < cols for ") + name);
+  if (M->rows && M->cols && !M->base) fail(MPFK_EINVAL, std::string("mpfk: null data for ") + name);
+}
+
+// check_mul_shapes, linalg.hpp:279-286
+void check_mul_shapes(const mpfk_mat* A, const mpfk_mat* B, const mpfk_mat* C) {
+  if (A->cols != B->rows) fail(MPFK_EINVAL, "matmul: inner dimensions differ");
+  if (C->rows != A->rows || C->cols != B->cols)
+    fail(MPFK_EINVAL, "matmul: result shape mismatch");
+}
+
+// check_n_min, linalg.hpp:290-294
+void check_n_min(uint64_t n_min, int variant) {
+  if (variant < MPFK_NORMAL || variant > MPFK_SIMD_LOADSTORE)
+    fail(MPFK_EINVAL, "matmul: unknown kernel variant");
+  if (n_min < 1) fail(MPFK_EINVAL, "matmul: n_min must be at least 1");
+  if (variant != MPFK_NORMAL && n_min % 4 != 0)
+    fail(MPFK_EINVAL, "matmul: SIMD variants need n_min divisible by 4");
+}
+
+uint64_t pad4(uint64_t c) { return (c + 3) & ~uint64_t(3); }
+
+// host pads of C -> +0 (zero_pads, linalg.hpp:99-106)
+void zero_host_pads(int W, mpfk_mat* C) {
+  if (C->stride == C->cols) return;
+  const uint64_t pc = plane_of(C);
+  for (int w = 0; w < W; ++w)
+    for (uint64_t i = 0; i < C->rows; ++i)
+      std::memset(C->base + w * pc + i * C->stride + C->cols, 0,
+                  (C->stride - C->cols) * sizeof(double));
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// One GPU's share of a host-buffer GEMM: rows [r0, r1) of C.
+struct Shard {
+  int dev;
+  uint64_t r0, r1;
+  uint64_t b0, b1;  // B rows this GPU uploads itself (G > 1: a 1/G slice)
+};
+
+// The multi-GPU host-buffer GEMM.  Device layout: planes packed with
+// ld = pad4(cols) (16-byte rows for cp.async), A shard rows only, full B.
+void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigned gpus) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const uint64_t m = A->rows, K = A->cols, n = B->cols;
+  mpfk_stats st{};
+  // fill_zero (linalg.hpp:94-96) semantics: every C cell is defined below;
+  // pads are cleared on the host.
+  if (m == 0 || n == 0) {
+    zero_host_pads(W, C);
+    count_matmul(m, n, K);
+    st.n_gpus = 0;
+    st.total_ms = ms_since(t0);
+    t_stats = st;
+    return;
+  }
+  ensure_devices((int)gpus);
+  int G = std::min<int>((int)gpus, g_ndev);
+  // never more GPUs than 64-row blocks, like nt = min(workers, nblocks)
+  G = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)G, (m + 63) / 64));
+  const uint64_t lda = pad4(K), ldb = pad4(n), ldc = pad4(n);
+  const uint64_t pa_h = plane_of(A), pb_h = plane_of(B), pc_h = plane_of(C);
+
+  // contiguous row spans rounded to 64 rows (the DD tile height)
+  std::vector<Shard> sh(G);
+  const uint64_t per = ((m + G - 1) / G + 63) / 64 * 64;
+  const uint64_t bper = (K + G - 1) / G;
+  for (int g = 0; g < G; ++g) {
+    sh[g].dev = g;
+    sh[g].r0 = std::min<uint64_t>(m, g * per);
+    sh[g].r1 = std::min<uint64_t>(m, (g + 1) * per);
+    sh[g].b0 = G == 1 ? 0 : std::min<uint64_t>(K, g * bper);
+    sh[g].b1 = G == 1 ? K : std::min<uint64_t>(K, (g + 1) * bper);
+  }
+  const bool peer = G > 1;
+  if (peer) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int a = 0; a < G; ++a) {
+      ck(cudaSetDevice(a), "cudaSetDevice");
+      for (int b = 0; b < G; ++b) {
+        if (a == b) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, a, b);
+        if (!can) fail(MPFK_ECUDA, "mpfk: GPUs lack peer access for the B all-gather");
+        cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "enable peer");
+        cudaGetLastError();
+      }
+    }
+  }
+
+  std::vector<float> h2d(G, 0.f), bc(G, 0.f), kms(G, 0.f), d2h(G, 0.f);
+  std::vector<int> launches(G, 0);
+  std::vector<std::exception_ptr> errs(G);
+  std::vector<Fail> fails(G);
+  std::vector<int> failed(G, 0);
+
+  auto phase1 = [&](int g) {  // allocate + upload A shard and B slice
+    Shard& s = sh[g];
+    Device& D = g_dev[s.dev];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    const uint64_t rows = s.r1 - s.r0;
+    grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(rows * lda, 1));
+    grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
+    grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(rows * ldc, 1));
+    ck(cudaEventRecord(D.ev[0], D.stream), "event");
+    for (int w = 0; w < W; ++w) {
+      if (rows && K)
+        ck(cudaMemcpy2DAsync(D.dA + w * rows * lda, lda * 8, A->base + w * pa_h + s.r0 * A->stride,
+                             A->stride * 8, K * 8, rows, cudaMemcpyHostToDevice, D.stream),
+           "H2D A");
+      if (s.b1 > s.b0 && n)
+        ck(cudaMemcpy2DAsync(D.dB + w * K * ldb + s.b0 * ldb, ldb * 8,
+                             B->base + w * pb_h + s.b0 * B->stride, B->stride * 8, n * 8,
+                             s.b1 - s.b0, cudaMemcpyHostToDevice, D.stream),
+           "H2D B");
+    }
+    ck(cudaEventRecord(D.ev[1], D.stream), "event");
+  };
+  auto phase2 = [&](int g) {  // gather the other B slices from peers, compute, download
+    Shard& s = sh[g];
+    Device& D = g_dev[s.dev];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    const uint64_t rows = s.r1 - s.r0;
+    if (peer) {
+      for (int o = 0; o < G; ++o) {
+        if (o == g || sh[o].b1 == sh[o].b0) continue;
+        Device& P = g_dev[sh[o].dev];
+        ck(cudaStreamWaitEvent(D.stream, P.ev[1], 0), "wait peer upload");
+        for (int w = 0; w < W; ++w)
+          ck(cudaMemcpyPeerAsync(D.dB + w * K * ldb + sh[o].b0 * ldb, s.dev,
+                                 P.dB + w * K * ldb + sh[o].b0 * ldb, sh[o].dev,
+                                 (sh[o].b1 - sh[o].b0) * ldb * 8, D.stream),
+             "peer copy B");
+      }
+    }
+    ck(cudaEventRecord(D.ev[2], D.stream), "event");
+    launches[g] = rows ? enqueue_gemm(W, rows, n, K, D.dA, lda, rows * lda, D.dB, ldb, K * ldb,
+                                      D.dC, ldc, rows * ldc, D.stream)
+                       : 0;
+    ck(cudaEventRecord(D.ev[3], D.stream), "event");
+    for (int w = 0; w < W; ++w)
+      if (rows)
+        ck(cudaMemcpy2DAsync(C->base + w * pc_h + s.r0 * C->stride, C->stride * 8,
+                             D.dC + w * rows * ldc, ldc * 8, n * 8, rows, cudaMemcpyDeviceToHost,
+                             D.stream),
+           "D2H C");
+    ck(cudaEventRecord(D.ev[4], D.stream), "event");
+    ck(cudaEventSynchronize(D.ev[4]), "GEMM execution");
+    cudaEventElapsedTime(&h2d[g], D.ev[0], D.ev[1]);
+    cudaEventElapsedTime(&bc[g], D.ev[1], D.ev[2]);
+    cudaEventElapsedTime(&kms[g], D.ev[2], D.ev[3]);
+    cudaEventElapsedTime(&d2h[g], D.ev[3], D.ev[4]);
+  };
+  auto run_all = [&](auto&& fn) {
+    if (G == 1) {
+      fn(0);
+      return;
+    }
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g)
+      th.emplace_back([&, g] {
+        try {
+          fn(g);
+        } catch (const Fail& f) {
+          fails[g] = f;
+          failed[g] = 1;
+        } catch (...) {
+          errs[g] = std::current_exception();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int g = 0; g < G; ++g) {
+      if (failed[g]) throw fails[g];
+      if (errs[g]) std::rethrow_exception(errs[g]);
+    }
+  };
+  int prev = 0;
+  cudaGetDevice(&prev);
+  run_all(phase1);
+  run_all(phase2);
+  cudaSetDevice(prev);
+
+  zero_host_pads(W, C);
+  count_matmul(m, n, K);
+  for (int g = 0; g < G; ++g) {
+    const uint64_t rows = sh[g].r1 - sh[g].r0;
+    st.h2d_ms = std::max<double>(st.h2d_ms, h2d[g]);
+    st.bcast_ms = std::max<double>(st.bcast_ms, bc[g]);
+    st.kernel_ms = std::max<double>(st.kernel_ms, kms[g]);
+    st.d2h_ms = std::max<double>(st.d2h_ms, d2h[g]);
+    st.h2d_bytes += 8ull * W * (rows * K + (sh[g].b1 - sh[g].b0) * n);
+    st.d2h_bytes += 8ull * W * rows * n;
+    st.peer_bytes += peer ? 8ull * W * (K - (sh[g].b1 - sh[g].b0)) * ldb : 0;
+    st.kernel_launches += launches[g];
+  }
+  st.n_gpus = G;
+  st.total_ms = ms_since(t0);
+  t_stats = st;
+}
+
+// ---------------------------------------------------------------------------
+// elementwise batch kernel for the arithmetic parity sweeps
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void binop_kernel(int op, long long count, const double* x, const double* y,
+                             double* r) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    double a[W], b[W], c[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) a[w] = x[i * W + w], b[w] = y[i * W + w];
+    if (op == 0)
+      arith::mp_add<W>(a, b, c);
+    else
+      arith::mp_mul<W>(a, b, c);
+#pragma unroll
+    for (int w = 0; w < W; ++w) r[i * W + w] = c[w];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FP64 pipe microbenchmark: 8 independent DFMA chains per thread
+// ---------------------------------------------------------------------------
+__global__ void fp64_peak_kernel(double* out, int iters, double m) {
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3 + j;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = __fma_rn(a[j], m, 1e-9);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  if (s == 12345.678) out[0] = s;
+}
+
+// ---------------------------------------------------------------------------
+// host generator; restated independently in
+// oracle/mpfk_oracle.c:orc_fill_baseline for cross-checking
+// ---------------------------------------------------------------------------
+struct SM64 {
+  uint64_t s;
+  uint64_t next() {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  double unit() { return static_cast<double>(next() >> 11) * 0x1p-53; }
+};
+
+// renormalized<W>(c, W): vec_sum then vseb(W) (mpf.hpp:76-88, eft.hpp:103-225)
+void renormalize_host(int W, const double* c, double* out) {
+  double d[4];
+  double s = c[W - 1];
+  for (int i = W - 1; i-- > 0;) {
+    double ss, e;
+    arith::two_sum(c[i], s, ss, e);
+    d[i + 1] = e;
+    s = ss;
+  }
+  d[0] = s;
+  for (int i = 0; i < W; ++i) out[i] = 0.0;
+  int j = 0;
+  double eps = d[0];
+  for (int i = 0; i + 1 < W; ++i) {
+    double ps, pe;
+    arith::qts(eps, d[i + 1], ps, pe);
+    out[j] = ps;
+    if (arith::nz(pe)) {
+      if (j >= W - 1) return;
+      ++j;
+      eps = pe;
+    } else {
+      eps = ps;
+    }
+  }
+  if (arith::nz(eps) && j < W) out[j] = eps;
+}
+
+void baseline_elem(int W, int wide, SM64& g, double* v) {
+  double c[4];
+  if (wide) {
+    const uint64_t sbits = g.next();
+    const int e = static_cast<int>(g.next() % 61ULL) - 30;
+    const double f = 1.0 + g.unit();
+    c[0] = std::ldexp((sbits & 1) ? -f : f, e);
+  } else {
+    c[0] = 2.0 * g.unit() - 1.0;
+  }
+  for (int i = 1; i < W; ++i) c[i] = (c[i - 1] * 0x1p-53) * (2.0 * g.unit() - 1.0);
+  if (W == 2)
+    arith::qts(c[0], c[1], v[0], v[1]);
+  else
+    renormalize_host(W, c, v);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int mpfk_abi_version(void) { return MPFK_ABI_VERSION; }
+
+const char* mpfk_last_error(void) { return t_err.c_str(); }
+
+int mpfk_device_count(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_ndev < 0) {
+    g_ndev = visible_sm100_devices();
+    g_dev.resize(std::max(g_ndev, 0));
+    for (int d = 0; d < g_ndev; ++d) g_dev[d].id = d;
+  }
+  return g_ndev;
+}
+
+int mpfk_init(int n_gpus) {
+  return guarded([&] { ensure_devices(n_gpus <= 0 ? 1 << 20 : n_gpus); });
+}
+
+void mpfk_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (auto& D : g_dev) {
+    if (!D.ready) continue;
+    cudaSetDevice(D.id);
+    cudaStreamSynchronize(D.stream);
+    if (D.dA) cudaFree(D.dA);
+    if (D.dB) cudaFree(D.dB);
+    if (D.dC) cudaFree(D.dC);
+    for (auto& e : D.ev) cudaEventDestroy(e);
+    cudaStreamDestroy(D.stream);
+    D = Device{};
+  }
+  g_dev.clear();
+  g_ndev = -1;
+  cudaSetDevice(prev);
+}
+
+int mpfk_selftest(void) {
+  return guarded([&] {
+    if (mpfk_device_count() == 0)
+      fail(MPFK_ENODEV, "mpfk: no CUDA sm_100 device is visible");
+    run_selftest_current();
+  });
+}
+
+int mpfk_matmul_block_parallel_into(int width, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B,
+                                    uint64_t n_min, int variant, unsigned workers) {
+  return guarded([&] {
+    check_width(width);
+    check_mat(A, "A");
+    check_mat(B, "B");
+    check_mat(C, "C");
+    check_mul_shapes(A, B, C);
+    check_n_min(n_min, variant);
+    if (workers < 1) fail(MPFK_EINVAL, "matmul: workers must be at least 1");
+    host_gemm(width, C, A, B, workers);
+  });
+}
+
+int mpfk_matmul_block_into(int width, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B,
+                           uint64_t n_min, int variant) {
+  return guarded([&] {
+    check_width(width);
+    check_mat(A, "A");
+    check_mat(B, "B");
+    check_mat(C, "C");
+    check_mul_shapes(A, B, C);
+    check_n_min(n_min, variant);
+    host_gemm(width, C, A, B, 1);
+  });
+}
+
+int mpfk_matmul_naive_into(int width, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B,
+                           int variant) {
+  return guarded([&] {
+    check_width(width);
+    check_mat(A, "A");
+    check_mat(B, "B");
+    check_mat(C, "C");
+    check_mul_shapes(A, B, C);
+    if (variant < MPFK_NORMAL || variant > MPFK_SIMD_LOADSTORE)
+      fail(MPFK_EINVAL, "matmul: unknown kernel variant");
+    host_gemm(width, C, A, B, 1);
+  });
+}
+
+int mpfk_last_stats(mpfk_stats* out) {
+  if (!out) return MPFK_EINVAL;
+  *out = t_stats;
+  return MPFK_OK;
+}
+
+int mpfk_gemm_device(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                     uint64_t a_plane, const double* B, uint64_t ldb, uint64_t b_plane, double* C,
+                     uint64_t ldc, uint64_t c_plane, void* stream, int* launches) {
+  return guarded([&] {
+    check_width(width);
+    if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
+    if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
+      fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+         reinterpret_cast<uintptr_t>(C)) & 15)
+      fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ensure_devices(dev + 1);
+    const int l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane,
+                               static_cast<cudaStream_t>(stream));
+    count_matmul(m, n, k);
+    if (launches) *launches = l;
+  });
+}
+
+int mpfk_binop_batch(int width, int op, uint64_t count, const double* x, const double* y,
+                     double* r) {
+  return guarded([&] {
+    check_width(width);
+    if (op != 0 && op != 1) fail(MPFK_EINVAL, "mpfk: op must be 0 (add) or 1 (mul)");
+    if (count == 0) return;
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ensure_devices(dev + 1);
+    const size_t bytes = sizeof(double) * width * count;
+    double *dx = nullptr, *dy = nullptr, *dr = nullptr;
+    ck(cudaMalloc(&dx, bytes), "cudaMalloc");
+    ck(cudaMalloc(&dy, bytes), "cudaMalloc");
+    ck(cudaMalloc(&dr, bytes), "cudaMalloc");
+    ck(cudaMemcpy(dx, x, bytes, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(dy, y, bytes, cudaMemcpyHostToDevice), "H2D");
+    const int blocks = (int)std::min<uint64_t>((count + 255) / 256, 148 * 16);
+    switch (width) {
+      case 2: binop_kernel<2><<<blocks, 256>>>(op, (long long)count, dx, dy, dr); break;
+      case 3: binop_kernel<3><<<blocks, 256>>>(op, (long long)count, dx, dy, dr); break;
+      case 4: binop_kernel<4><<<blocks, 256>>>(op, (long long)count, dx, dy, dr); break;
+    }
+    ck(cudaGetLastError(), "binop launch");
+    ck(cudaMemcpy(r, dr, bytes, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dr);
+  });
+}
+
+void mpfk_op_counters_reset(void) {
+  g_adds.store(0, std::memory_order_relaxed);
+  g_muls.store(0, std::memory_order_relaxed);
+  g_leaf.store(0, std::memory_order_relaxed);
+}
+
+void mpfk_op_counters_read(uint64_t* adds, uint64_t* muls, uint64_t* leaf) {
+  if (adds) *adds = g_adds.load(std::memory_order_relaxed);
+  if (muls) *muls = g_muls.load(std::memory_order_relaxed);
+  if (leaf) *leaf = g_leaf.load(std::memory_order_relaxed);
+}
+
+void* mpfk_host_alloc(uint64_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 1;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    t_err = "mpfk: cudaMallocHost failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void mpfk_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int mpfk_fill_baseline(int width, int wide, uint64_t row0, uint64_t rows, uint64_t cols,
+                       uint64_t stride, uint64_t seed, double* planes, int threads) {
+  return guarded([&] {
+    check_width(width);
+    if (stride < cols) fail(MPFK_EINVAL, "mpfk: stride < cols");
+    if (rows && cols && !planes) fail(MPFK_EINVAL, "mpfk: null planes");
+    unsigned T = threads > 0 ? (unsigned)threads : std::max(1u, std::thread::hardware_concurrency());
+    T = (unsigned)std::min<uint64_t>(T, std::max<uint64_t>(rows, 1));
+    const uint64_t ps = rows * stride;
+    auto body = [&](unsigned t) {
+      for (uint64_t i = t; i < rows; i += T) {
+        SM64 g{seed ^ ((row0 + i + 1) * 0xd1b54a32d192ed03ULL)};
+        for (uint64_t j = 0; j < cols; ++j) {
+          double v[4];
+          baseline_elem(width, wide, g, v);
+          for (int w = 0; w < width; ++w) planes[w * ps + i * stride + j] = v[w];
+        }
+        for (int w = 0; w < width; ++w)
+          for (uint64_t j = cols; j < stride; ++j) planes[w * ps + i * stride + j] = 0.0;
+      }
+    };
+    if (T <= 1) {
+      body(0);
+      return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; ++t) th.emplace_back(body, t);
+    for (auto& x : th) x.join();
+  });
+}
+
+int mpfk_fp64_peak(double* ops_per_s, double* ms_out) {
+  return guarded([&] {
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ensure_devices(dev + 1);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* d = nullptr;
+    ck(cudaMalloc(&d, 8), "cudaMalloc");
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    fp64_peak_kernel<<<blocks, threads>>>(d, iters, 0.999999);  // warm-up
+    ck(cudaGetLastError(), "fp64 peak launch");
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+      cudaEventRecord(a);
+      fp64_peak_kernel<<<blocks, threads>>>(d, iters, 0.999999);
+      cudaEventRecord(b);
+      ck(cudaEventSynchronize(b), "fp64 peak");
+      float t = 0;
+      cudaEventElapsedTime(&t, a, b);
+      best = std::min(best, t);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    const double ops = double(blocks) * threads * iters * 8.0;
+    if (ops_per_s) *ops_per_s = ops / (best * 1e-3);
+    if (ms_out) *ms_out = best;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+// gemm_kernel.cuh -- register-blocked, shared-memory-tiled DD/TD/QD GEMM for
+// sm_100a on the FP64 CUDA-core pipe.
+//
+// Replaces the reference's hot loop: matmul_block*_into -> mul_panel ->
+// QuadRow::axpy -> mpf::mul/add<W> (linalg.hpp:250-277, 368-433).
+//
+// Per-element contract (linalg.hpp:235-248, 338-344): C(i,j) = mul(A(i,0),
+// B(0,j)); then C(i,j) = add(C(i,j), mul(A(i,k), B(k,j))) for k = 1..K-1 in
+// ascending order.  Each thread owns a TM x TN register micro-tile of all W
+// components and walks k in exactly that order, so every C element is
+// bit-identical to the reference for any tiling, grid or GPU count.  K is
+// never padded (an extra add(C, mul(0, b)) is not a bitwise identity on
+// signed zeros), the k loop is bounded by the true K.
+//
+// Data movement: A and B tiles of all W component planes (the reference's
+// SoA layout, linalg.hpp:36-129) are staged into shared memory with 16-byte
+// cp.async (LDGSTS) in a STAGES-deep ring; operand traffic is tiny next to
+// the 20-218 FP64 operations per multiply-add, so the kernel is bound by the
+// FP64 pipe, not by HBM, L2 or shared memory.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mpf_arith.cuh"
+
+namespace mpfk {
+namespace kern {
+
+struct GemmArgs {
+  const double* A;  // W planes, plane stride pa, row stride lda (elements)
+  const double* B;
+  double* C;
+  long long lda, ldb, ldc;
+  long long pa, pb, pc;
+  int M, N, K;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;  // src-size 0 -> 16 zero bytes, no global read
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1>
+struct TileCfg {
+  static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
+  static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_;
+  static constexpr int TX = BN / TN;  // threads along N
+  static constexpr int TY = BM / TM;  // threads along M
+  static constexpr int THREADS = TX * TY;
+  static constexpr int APAD = 2, BPAD = 2;  // keep 16 B row alignment, spread banks
+  static constexpr int AS = BK + APAD;      // A tile row stride (doubles), [BM][AS]
+  static constexpr int BS = BN + BPAD;      // B tile row stride, [BK][BS]
+  static constexpr int A_STAGE = W * BM * AS;
+  static constexpr int B_STAGE = W * BK * BS;
+  static constexpr size_t SMEM = sizeof(double) * size_t(STAGES) * (A_STAGE + B_STAGE);
+  static_assert(BK % 2 == 0 && BN % 2 == 0, "16-byte chunks");
+  static_assert(BM % TM == 0 && BN % TN == 0, "micro-tile");
+};
+
+template <class Cfg>
+__device__ __forceinline__ void load_tile(double* As, double* Bs, const GemmArgs& g, int m0,
+                                          int n0, int k0) {
+  constexpr int W = Cfg::W, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
+  const int tid = threadIdx.x;
+  // A: BM rows x BK/2 chunks per plane
+  constexpr int ACH = BM * (BK / 2);
+#pragma unroll
+  for (int c = tid; c < W * ACH; c += Cfg::THREADS) {
+    const int w = c / ACH, r = (c % ACH) / (BK / 2), kc = (c % ACH) % (BK / 2);
+    const int gm = m0 + r, gk = k0 + 2 * kc;
+    const bool ok = gm < g.M && gk < g.K;
+    const double* src = ok ? g.A + w * g.pa + (long long)gm * g.lda + gk : g.A;
+    cp_async16(As + w * BM * Cfg::AS + r * Cfg::AS + 2 * kc, src, ok);
+  }
+  constexpr int BCH = BK * (BN / 2);
+#pragma unroll
+  for (int c = tid; c < W * BCH; c += Cfg::THREADS) {
+    const int w = c / BCH, r = (c % BCH) / (BN / 2), nc = (c % BCH) % (BN / 2);
+    const int gk = k0 + r, gn = n0 + 2 * nc;
+    const bool ok = gk < g.K && gn < g.N;
+    const double* src = ok ? g.B + w * g.pb + (long long)gk * g.ldb + gn : g.B;
+    cp_async16(Bs + w * BK * Cfg::BS + r * Cfg::BS + 2 * nc, src, ok);
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS)
+    mpgemm_kernel(const GemmArgs g) {
+  constexpr int W = Cfg::W, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
+  constexpr int TM = Cfg::TM, TN = Cfg::TN, TX = Cfg::TX, TY = Cfg::TY;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ __align__(16) double smem[];
+  double* As0 = smem;
+  double* Bs0 = smem + STAGES * Cfg::A_STAGE;
+
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int ktiles = (g.K + BK - 1) / BK;
+
+  double acc[TM][TN][W];
+
+  // prologue: fill STAGES-1 stages
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_tile<Cfg>(As0 + s * Cfg::A_STAGE, Bs0 + s * Cfg::B_STAGE, g, m0, n0, s * BK);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    // issue the tile STAGES-1 ahead into the slot freed last iteration
+    {
+      const int nt = kt + STAGES - 1;
+      if (nt < ktiles) {
+        const int slot = nt % STAGES;
+        load_tile<Cfg>(As0 + slot * Cfg::A_STAGE, Bs0 + slot * Cfg::B_STAGE, g, m0, n0, nt * BK);
+      }
+      cp_async_commit();
+    }
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+
+    const int slot = kt % STAGES;
+    const double* As = As0 + slot * Cfg::A_STAGE;
+    const double* Bs = Bs0 + slot * Cfg::B_STAGE;
+    const int kend = min(BK, g.K - kt * BK);
+    int kk = 0;
+    if (kt == 0) {
+      // k == 0: the product initialises the element (linalg.hpp:242, 260-261)
+      double a[TM][W], b[TN][W];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS];
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + tx + j * TX];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) arith::mp_mul<W>(a[i], b[j], acc[i][j]);
+      kk = 1;
+    }
+#pragma unroll Cfg::KUNROLL
+    for (; kk < kend; ++kk) {
+      double a[TM][W], b[TN][W];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + kk * Cfg::BS + tx + j * TX];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          double p[W];
+          arith::mp_mul<W>(a[i], b[j], p);
+          arith::mp_add<W>(acc[i][j], p, acc[i][j]);
+        }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  if (ktiles == 0) return;  // K == 0 is handled by the host (C = +0)
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int gm = m0 + ty + i * TY;
+    if (gm >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int gn = n0 + tx + j * TX;
+      if (gn >= g.N) continue;
+#pragma unroll
+      for (int w = 0; w < W; ++w) g.C[w * g.pc + (long long)gm * g.ldc + gn] = acc[i][j][w];
+    }
+  }
+}
+
+}  // namespace kern
+}  // namespace mpfk

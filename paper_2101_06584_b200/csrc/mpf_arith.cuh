@@ -1,0 +1,315 @@
+// mpf_arith.cuh -- DD/TD/QD arithmetic as device-inlined SIMT FP64 code.
+//
+// B200-native restatement of the reference's error-free transformations and
+// width kernels (mpfkit: proj/include/mpfkit/eft.hpp, mpf.hpp).  Every
+// function reproduces the reference's operation sequence exactly, so results
+// are bit-identical to the CPU library; the only structural change is that
+// the branchy renormalisation steps (renorm5, vseb) are restated as
+// predicated selects so a warp does not diverge on the common path.
+//
+// The same source compiles for the host (g++/nvcc host pass, with
+// -ffp-contract=off) so tests/test_arith_host.py can check it bit-for-bit
+// against the reference build before any GPU time is spent.  On the device
+// every rounding operation is an explicit __dadd_rn/__dsub_rn/__dmul_rn/
+// __fma_rn intrinsic: nvcc never contracts those into DFMA, regardless of
+// -fmad (default contraction breaks the EFTs).
+#pragma once
+
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define MPFK_HD __host__ __device__ __forceinline__
+#else
+#define MPFK_HD inline __attribute__((always_inline))
+#include <cmath>
+#include <cstring>
+#endif
+
+namespace mpfk {
+namespace arith {
+
+// ---------------------------------------------------------------------------
+// Rounded binary64 operations (the "policy" of eft.hpp:29-31).
+// ---------------------------------------------------------------------------
+#if defined(__CUDA_ARCH__)
+MPFK_HD double add(double a, double b) { return __dadd_rn(a, b); }
+MPFK_HD double sub(double a, double b) { return __dsub_rn(a, b); }
+MPFK_HD double mul(double a, double b) { return __dmul_rn(a, b); }
+MPFK_HD double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+// x != 0 (either sign of zero counts as zero) as an integer test on the bit
+// pattern: one LOP3 + ISETP on the ALU pipe instead of a DSETP on the FP64
+// pipe, which is the bottleneck.
+MPFK_HD bool nz(double x) {
+  return ((__double2hiint(x) & 0x7fffffff) | __double2loint(x)) != 0;
+}
+#else
+MPFK_HD double add(double a, double b) { return a + b; }
+MPFK_HD double sub(double a, double b) { return a - b; }
+MPFK_HD double mul(double a, double b) { return a * b; }
+MPFK_HD double fma(double a, double b, double c) { return std::fma(a, b, c); }
+MPFK_HD bool nz(double x) {
+  uint64_t u;
+  std::memcpy(&u, &x, sizeof u);
+  return (u << 1) != 0;
+}
+#endif
+MPFK_HD double sel(bool p, double a, double b) { return p ? a : b; }
+
+// ---------------------------------------------------------------------------
+// EFT primitives, eft.hpp:46-113.
+// ---------------------------------------------------------------------------
+
+// Knuth two-sum, eft.hpp:46-51 (6 ops).
+MPFK_HD void two_sum(double a, double b, double& s, double& e) {
+  const double ss = add(a, b);
+  const double v = sub(ss, a);
+  e = add(sub(a, sub(ss, v)), sub(b, v));
+  s = ss;
+}
+
+// Dekker fast-two-sum, eft.hpp:55-59 (3 ops).
+MPFK_HD void qts(double a, double b, double& s, double& e) {
+  const double ss = add(a, b);
+  e = sub(b, sub(ss, a));
+  s = ss;
+}
+
+// FMA two-product, eft.hpp:63-67: e = fma(a, b, -s).  The negation is an
+// exact sign flip folded into the DFMA operand.
+MPFK_HD void two_prod(double a, double b, double& s, double& e) {
+  const double ss = mul(a, b);
+  e = fma(a, b, -ss);
+  s = ss;
+}
+
+// three-sum, eft.hpp:87-92.
+MPFK_HD void three_sum(double a, double b, double c, double& s, double& e1, double& e2) {
+  double ts, te, us, ue;
+  two_sum(a, b, ts, te);
+  two_sum(c, ts, us, ue);
+  two_sum(te, ue, e1, e2);
+  s = us;
+}
+
+// three-sum2, eft.hpp:95-99.
+MPFK_HD void three_sum2(double a, double b, double c, double& s, double& e) {
+  double ts, te, us, ue;
+  two_sum(a, b, ts, te);
+  two_sum(c, ts, us, ue);
+  s = us;
+  e = add(te, ue);
+}
+
+// ---------------------------------------------------------------------------
+// renorm5, eft.hpp:241-288.
+//
+// Backward quick-two-sum sweep, then the forward emission.  Paths A and B of
+// the reference (first two forward residuals nonzero) cover >99% of GEMM MACs
+// on random inputs; they differ only in where the last
+// term lands, which is a select.  The remaining paths (a zero residual in the
+// first two forward steps -- structured or sparse inputs) take the reference's
+// branch structure verbatim.
+//
+// Signed zeros: every slot the reference leaves untouched keeps its exact
+// value, including the +0 initialisers of s2/s3 (eft.hpp:251).
+// ---------------------------------------------------------------------------
+MPFK_HD void renorm5(double c0, double c1, double c2, double c3, double c4, double& r0,
+                     double& r1, double& r2, double& r3) {
+  double t;
+  qts(c3, c4, t, c4);
+  qts(c2, t, t, c3);
+  qts(c1, t, t, c2);
+  qts(c0, t, c0, c1);
+
+  double s0, s1, u, s2;
+  qts(c0, c1, s0, s1);
+  qts(s1, c2, u, s2);
+  if (nz(s1) & nz(s2)) {
+    // path A (s3 != 0: s3 += c4) or path B (s3 == 0: s2 += c4), eft.hpp:255-260
+    double v, s3;
+    qts(s2, c3, v, s3);
+    const bool p = nz(s3);
+    const double acc = add(sel(p, s3, v), c4);
+    r0 = s0;
+    r1 = u;
+    r2 = sel(p, v, acc);
+    r3 = sel(p, acc, s3);
+    return;
+  }
+  // paths C/D and the zero-residual corners, eft.hpp:261-286, verbatim
+  s2 = 0.0;
+  double s3 = 0.0;
+  if (nz(s1)) {
+    // here the residual of qts(s1, c2) was zero: eft.hpp:261-268
+    s1 = u;
+    qts(s1, c3, s1, s2);
+    if (nz(s2)) {
+      qts(s2, c4, s2, s3);
+    } else {
+      qts(s1, c4, s1, s2);
+    }
+  } else {
+    qts(s0, c2, s0, s1);
+    if (nz(s1)) {
+      qts(s1, c3, s1, s2);
+      if (nz(s2)) {
+        qts(s2, c4, s2, s3);
+      } else {
+        qts(s1, c4, s1, s2);
+      }
+    } else {
+      qts(s0, c3, s0, s1);
+      if (nz(s1)) {
+        qts(s1, c4, s1, s2);
+      } else {
+        qts(s0, c4, s0, s1);
+      }
+    }
+  }
+  r0 = s0, r1 = s1, r2 = s2, r3 = s3;
+}
+
+// vseb with k = 2 output slots over n = 3 inputs (the only use on the path:
+// td_mul, mpf.hpp:162), eft.hpp:205-225 unrolled:
+//   (a, r) = qts(e1, e2); eps = r != 0 ? r : a; (b, r2) = qts(eps, e3)
+//   r != 0: out = (a, b)
+//   r == 0: out = (b, r2 != 0 ? r2 : +0)    (a zero residual never lands)
+MPFK_HD void vseb_2_3(double e1, double e2, double e3, double& o1, double& o2) {
+  double a, r, b, r2;
+  qts(e1, e2, a, r);
+  const bool p = nz(r);
+  qts(sel(p, r, a), e3, b, r2);
+  o1 = sel(p, a, b);
+  o2 = sel(p, b, sel(nz(r2), r2, 0.0));
+}
+
+// ---------------------------------------------------------------------------
+// Width kernels, mpf.hpp:105-238.  Arrays are component-major (c[0] leads).
+// ---------------------------------------------------------------------------
+
+// dd_add, mpf.hpp:105-111 (11 ops).
+MPFK_HD void dd_add(const double* x, const double* y, double* r) {
+  double s, e;
+  two_sum(x[0], y[0], s, e);
+  const double w = add(x[1], y[1]);
+  e = add(e, w);
+  qts(s, e, r[0], r[1]);
+}
+
+// dd_mul, mpf.hpp:113-119 (9 ops; the cross terms are a plain mul+mul+add,
+// not an fma).
+MPFK_HD void dd_mul(const double* x, const double* y, double* r) {
+  double p, e;
+  two_prod(x[0], y[0], p, e);
+  const double w = add(mul(x[0], y[1]), mul(x[1], y[0]));
+  e = add(e, w);
+  qts(p, e, r[0], r[1]);
+}
+
+// qd_add, mpf.hpp:178-196 (63 ops + renorm5).  With Trunc3 the fourth
+// output is not produced (td_add_q drops it, mpf.hpp:141), which lets the
+// compiler delete the dead tail of renorm5.
+template <bool Trunc3 = false>
+MPFK_HD void qd_add(const double* x, const double* y, double* r) {
+  double s0, t0, s1, t1, s2, t2, s3, t3;
+  two_sum(x[0], y[0], s0, t0);
+  two_sum(x[1], y[1], s1, t1);
+  two_sum(x[2], y[2], s2, t2);
+  two_sum(x[3], y[3], s3, t3);
+  two_sum(s1, t0, s1, t0);
+  three_sum(s2, t0, t1, s2, t0, t1);
+  three_sum2(s3, t0, t2, s3, t0);
+  t0 = add(add(t0, t1), t3);
+  double r3;
+  renorm5(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3);
+  if (!Trunc3) r[3] = r3;
+}
+
+// qd_mul, mpf.hpp:198-238 (111 ops + renorm5), including the pre-combined
+// operand pairs that keep it bitwise commutative (mpf.hpp:214-221).
+MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
+  double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
+  two_prod(x[0], y[0], p0, q0);
+  two_prod(x[0], y[1], p1, q1);
+  two_prod(x[1], y[0], p2, q2);
+  two_prod(x[0], y[2], p3, q3);
+  two_prod(x[1], y[1], p4, q4);
+  two_prod(x[2], y[0], p5, q5);
+
+  three_sum(p1, p2, q0, p1, p2, q0);
+  double gs, ge;
+  two_sum(q1, q2, gs, ge);
+  three_sum(p2, gs, ge, p2, q1, q2);
+  double hs, he;
+  two_sum(p3, p5, hs, he);
+  three_sum(hs, p4, he, p3, p4, p5);
+
+  double s0, t0, s1, t1;
+  two_sum(p2, p3, s0, t0);
+  two_sum(q1, p4, s1, t1);
+  double s2 = add(q2, p5);
+  two_sum(s1, t0, s1, t0);
+  s2 = add(s2, add(t0, t1));
+  s1 = add(s1, add(mul(x[0], y[3]), mul(x[3], y[0])));
+  s1 = add(s1, add(mul(x[1], y[2]), mul(x[2], y[1])));
+  s1 = add(s1, q0);
+  s1 = add(s1, add(q3, q5));
+  s1 = add(s1, q4);
+  renorm5(p0, p1, s0, s1, s2, r[0], r[1], r[2], r[3]);
+}
+
+// td_add_q, mpf.hpp:135-142: zero-extend with +0, quad add, truncate.
+MPFK_HD void td_add_q(const double* x, const double* y, double* r) {
+  const double xx[4] = {x[0], x[1], x[2], 0.0};
+  const double yy[4] = {y[0], y[1], y[2], 0.0};
+  qd_add<true>(xx, yy, r);
+}
+
+// td_mul, mpf.hpp:146-163 (41 ops + vseb).
+MPFK_HD void td_mul(const double* x, const double* y, double* r) {
+  double z00s, z00e, z01s, z01e, z10s, z10e;
+  two_prod(x[0], y[0], z00s, z00e);
+  two_prod(x[0], y[1], z01s, z01e);
+  two_prod(x[1], y[0], z10s, z10e);
+  // vec_sum<3>(z00.e, z01.s, z10.s), eft.hpp:103-113
+  double b0, b1, b2, s;
+  two_sum(z01s, z10s, s, b2);
+  two_sum(z00e, s, b0, b1);
+  const double c = fma(x[1], y[1], b2);
+  const double z31 = fma(x[0], y[2], z10e);
+  const double z32 = fma(x[2], y[0], z01e);
+  const double z3 = add(z31, z32);
+  const double s3 = add(c, z3);
+  // vec_sum<4>(z00.s, b0, b1, s3)
+  double e0, e1, e2, e3;
+  two_sum(b1, s3, s, e3);
+  two_sum(b0, s, s, e2);
+  two_sum(z00s, s, e0, e1);
+  r[0] = e0;
+  vseb_2_3(e1, e2, e3, r[1], r[2]);
+}
+
+// Library width defaults, mpf.hpp:242-260.
+template <int W>
+MPFK_HD void mp_add(const double* x, const double* y, double* r) {
+  if constexpr (W == 2) dd_add(x, y, r);
+  else if constexpr (W == 3) td_add_q(x, y, r);
+  else qd_add<false>(x, y, r);
+}
+
+template <int W>
+MPFK_HD void mp_mul(const double* x, const double* y, double* r) {
+  if constexpr (W == 2) dd_mul(x, y, r);
+  else if constexpr (W == 3) td_mul(x, y, r);
+  else qd_mul(x, y, r);
+}
+
+// Algorithmic FP64 operations per multiply-add (reference sequence, renorm5
+// path A): the roofline numerator.
+template <int W>
+constexpr int ops_per_mac() {
+  return W == 2 ? 20 : (W == 3 ? 132 : 218);
+}
+
+}  // namespace arith
+}  // namespace mpfk

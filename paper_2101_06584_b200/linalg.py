@@ -1,0 +1,275 @@
+"""Python mirror of the reference's matrix API (mpfkit::linalg,
+/root/reference/proj/include/mpfkit/linalg.hpp) over libmpfk.
+
+Same names, argument meaning and error behaviour as the reference:
+  MPMatrix(W, rows, cols)                 MPMatrix<W> (linalg.hpp:36-129)
+  pad_columns(cols)                       linalg.hpp:32-34
+  bits_equal(a, b)                        linalg.hpp:132-140
+  KernelVariant.{NORMAL,SIMD_SET,SIMD_LOADSTORE}   linalg.hpp:149
+  matmul_naive[_into], matmul_block[_into], matmul_block_parallel[_into]
+                                          linalg.hpp:346-443
+  op_counters_reset / op_counters_read    linalg.hpp:160-170, linalg.cpp:13-25
+std::invalid_argument surfaces as ValueError with the reference's message.
+The `workers` argument of the parallel form is the number of GPUs (capped by
+the visible devices); C is sharded by contiguous row spans exactly like the
+reference's worker partition, and the result is bit-identical for any count.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from collections import namedtuple
+
+import numpy as np
+
+from . import _native as N
+
+
+class KernelVariant(enum.IntEnum):
+    NORMAL = 0
+    SIMD_SET = 1
+    SIMD_LOADSTORE = 2
+
+
+OpCounts = namedtuple("OpCounts", "adds muls leaf_multiplies")
+
+
+def pad_columns(cols: int) -> int:
+    return (cols + 3) & ~3
+
+
+def format_eps(W: int) -> float:
+    """mpf::format_eps<W>, mpf.hpp:48-53."""
+    return {2: 2.0 ** -104, 3: 2.0 ** -157, 4: 2.0 ** -209}[W]
+
+
+class _Pinned:
+    """Owner of a page-locked host allocation (mpfk_host_alloc)."""
+
+    def __init__(self, nbytes):
+        self.ptr = N.lib().mpfk_host_alloc(nbytes)
+        if not self.ptr:
+            raise MemoryError(N.last_error())
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                N.lib().mpfk_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+class MPMatrix:
+    """Component-planar width-W matrix: W planes of rows x stride binary64,
+    stride = pad_columns(cols), padding cells +0 (linalg.hpp:25-34).
+
+    ``data`` is a (W, rows, stride) float64 numpy array.  ``pinned=True``
+    places it in page-locked memory so host<->device copies run at full
+    PCIe speed (the e2e path of bench.py)."""
+
+    def __init__(self, W: int, rows: int = 0, cols: int = 0, pinned: bool = False):
+        if W not in (2, 3, 4):
+            raise ValueError("MPMatrix: width must be 2, 3 or 4")
+        self.W = W
+        self._rows, self._cols = int(rows), int(cols)
+        self._stride = pad_columns(self._cols)
+        shape = (W, self._rows, self._stride)
+        self._owner = None
+        if pinned and self._rows * self._stride > 0:
+            nbytes = 8 * W * self._rows * self._stride
+            self._owner = _Pinned(nbytes)
+            buf = (C.c_double * (nbytes // 8)).from_address(self._owner.ptr)
+            self.data = np.frombuffer(buf, dtype=np.float64).reshape(shape)
+            self.data[...] = 0.0
+        else:
+            self.data = np.zeros(shape, dtype=np.float64)
+
+    # --- reference accessors -------------------------------------------------
+    def rows(self):
+        return self._rows
+
+    def cols(self):
+        return self._cols
+
+    def stride(self):
+        return self._stride
+
+    def plane_size(self):
+        return self._rows * self._stride
+
+    def plane(self, w: int):
+        if not 0 <= w < self.W:
+            raise ValueError("MPMatrix::plane: component out of range")
+        return self.data[w]
+
+    def at(self, i: int, j: int):
+        if not (0 <= i < self._rows and 0 <= j < self._cols):
+            raise ValueError("MPMatrix::at: index out of range")
+        return tuple(float(self.data[w, i, j]) for w in range(self.W))
+
+    def set(self, i: int, j: int, v):
+        if not (0 <= i < self._rows and 0 <= j < self._cols):
+            raise ValueError("MPMatrix::set: index out of range")
+        for w in range(self.W):
+            self.data[w, i, j] = v[w]
+
+    def same_shape(self, o: "MPMatrix") -> bool:
+        return self._rows == o._rows and self._cols == o._cols
+
+    def fill_zero(self):
+        self.data[...] = 0.0
+
+    def zero_pads(self):
+        self.data[:, :, self._cols:] = 0.0
+
+    def copy(self, pinned: bool = False) -> "MPMatrix":
+        m = MPMatrix(self.W, self._rows, self._cols, pinned=pinned)
+        m.data[...] = self.data
+        return m
+
+    # --- numpy interop -------------------------------------------------------
+    @classmethod
+    def from_planes(cls, planes, pinned: bool = False) -> "MPMatrix":
+        """planes: (W, rows, cols) float64 array-like."""
+        p = np.asarray(planes, dtype=np.float64)
+        W, r, c = p.shape
+        m = cls(W, r, c, pinned=pinned)
+        m.data[:, :, :c] = p
+        return m
+
+    def planes(self):
+        """(W, rows, cols) view without padding."""
+        return self.data[:, :, : self._cols]
+
+    def _c(self) -> N.MpfkMat:
+        return N.MpfkMat(self.data.ctypes.data if self.data.size else None, self._rows, self._cols,
+                         self._stride, self._rows * self._stride)
+
+
+def bits_equal(a: MPMatrix, b: MPMatrix) -> bool:
+    """Full-representation equality, padding included (linalg.hpp:132-140)."""
+    if a.W != b.W or not a.same_shape(b):
+        return False
+    return a.data.view(np.uint64).tobytes() == b.data.view(np.uint64).tobytes()
+
+
+def _check_same_width(*ms):
+    W = ms[0].W
+    for m in ms:
+        if m.W != W:
+            raise ValueError("matmul: operands must share one width")
+    return W
+
+
+def matmul_block_parallel_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix, n_min: int = 32,
+                               variant: KernelVariant = KernelVariant.NORMAL, workers: int = 1):
+    """linalg.hpp:402-433 on min(workers, GPUs) devices."""
+    W = _check_same_width(C_, A, B)
+    if workers < 1:
+        raise ValueError("matmul: workers must be at least 1")
+    if n_min < 0:
+        raise ValueError("matmul: n_min must be at least 1")
+    c, a, b = C_._c(), A._c(), B._c()
+    N.check(N.lib().mpfk_matmul_block_parallel_into(W, C.byref(c), C.byref(a), C.byref(b), int(n_min),
+                                                    int(variant), int(workers)))
+
+
+def matmul_block_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix, n_min: int = 32,
+                      variant: KernelVariant = KernelVariant.NORMAL):
+    """linalg.hpp:368-388."""
+    W = _check_same_width(C_, A, B)
+    if n_min < 0:
+        raise ValueError("matmul: n_min must be at least 1")
+    c, a, b = C_._c(), A._c(), B._c()
+    N.check(N.lib().mpfk_matmul_block_into(W, C.byref(c), C.byref(a), C.byref(b), int(n_min), int(variant)))
+
+
+def matmul_naive_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix,
+                      variant: KernelVariant = KernelVariant.NORMAL):
+    """linalg.hpp:346-358."""
+    W = _check_same_width(C_, A, B)
+    c, a, b = C_._c(), A._c(), B._c()
+    N.check(N.lib().mpfk_matmul_naive_into(W, C.byref(c), C.byref(a), C.byref(b), int(variant)))
+
+
+def matmul_block_parallel(A: MPMatrix, B: MPMatrix, n_min: int = 32,
+                          variant: KernelVariant = KernelVariant.NORMAL, workers: int = 1,
+                          pinned: bool = False) -> MPMatrix:
+    C_ = MPMatrix(A.W, A.rows(), B.cols(), pinned=pinned)
+    matmul_block_parallel_into(C_, A, B, n_min, variant, workers)
+    return C_
+
+
+def matmul_block(A: MPMatrix, B: MPMatrix, n_min: int = 32,
+                 variant: KernelVariant = KernelVariant.NORMAL) -> MPMatrix:
+    C_ = MPMatrix(A.W, A.rows(), B.cols())
+    matmul_block_into(C_, A, B, n_min, variant)
+    return C_
+
+
+def matmul_naive(A: MPMatrix, B: MPMatrix, variant: KernelVariant = KernelVariant.NORMAL) -> MPMatrix:
+    C_ = MPMatrix(A.W, A.rows(), B.cols())
+    matmul_naive_into(C_, A, B, variant)
+    return C_
+
+
+def op_counters_reset():
+    N.lib().mpfk_op_counters_reset()
+
+
+def op_counters_read() -> OpCounts:
+    a, m, l_ = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    N.lib().mpfk_op_counters_read(C.byref(a), C.byref(m), C.byref(l_))
+    return OpCounts(a.value, m.value, l_.value)
+
+
+def last_stats() -> dict:
+    s = N.MpfkStats()
+    N.check(N.lib().mpfk_last_stats(C.byref(s)))
+    return s.as_dict()
+
+
+# --- device-resident operands ---------------------------------------------------
+
+def gemm_device(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int, ldb: int,
+                b_plane: int, C_ptr: int, ldc: int, c_plane: int, stream: int = 0) -> int:
+    """Enqueue C = A*B on the current device/stream (mpfk_gemm_device).
+    Returns the number of kernel launches."""
+    launches = C.c_int(0)
+    N.check(N.lib().mpfk_gemm_device(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
+                                     c_plane, stream or None, C.byref(launches)))
+    return launches.value
+
+
+def binop_batch(W: int, op: str, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Elementwise mpf::add/mul<W> on the GPU over (count, W) arrays."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if x.shape != y.shape or x.ndim != 2 or x.shape[1] != W:
+        raise ValueError("binop_batch: x and y must be (count, W)")
+    r = np.empty_like(x)
+    N.check(N.lib().mpfk_binop_batch(W, {"add": 0, "mul": 1}[op], x.shape[0], x.ctypes.data, y.ctypes.data,
+                                     r.ctypes.data))
+    return r
+
+
+def fill_baseline(W: int, rows: int, cols: int, seed: int, wide: bool = False, pinned: bool = False,
+                  threads: int = 0, row0: int = 0) -> MPMatrix:
+    """BASELINE.json inputs (include/mpfk.h: mpfk_fill_baseline): rows
+    [row0, row0 + rows) of the seeded matrix."""
+    m = MPMatrix(W, rows, cols, pinned=pinned)
+    if rows and cols:
+        N.check(N.lib().mpfk_fill_baseline(W, int(bool(wide)), row0, rows, cols, m.stride(),
+                                           seed & (2 ** 64 - 1), m.data.ctypes.data, threads))
+    return m
+
+
+def fp64_peak() -> tuple:
+    """(FP64 lane-ops/s, ms) measured on the current device."""
+    ops, ms = C.c_double(), C.c_double()
+    N.check(N.lib().mpfk_fp64_peak(C.byref(ops), C.byref(ms)))
+    return ops.value, ms.value
+
+
+def device_count() -> int:
+    return N.lib().mpfk_device_count()

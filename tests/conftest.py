@@ -1,0 +1,23 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA sm_100 device (run on the B200 box)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def gpu_lib():
+    """libmpfk with at least one usable device; GPU tests fail (not skip)
+    when the library or the device is missing: there is no fallback."""
+    import paper_2101_06584_b200 as P
+    n = P.device_count()
+    assert n >= 1, "no CUDA sm_100 device visible to libmpfk"
+    return P

@@ -1,0 +1,70 @@
+// arith_host.cpp -- TEST SHIM: the product's device arithmetic header
+// (paper_2101_06584_b200/csrc/mpf_arith.cuh) compiled for the host with
+// -ffp-contract=off, so tests/test_arith_host.py can compare the exact same
+// source against the reference build (oracle/_ref) on millions of inputs
+// without a GPU.  The device build uses __dadd_rn & co. with identical IEEE
+// semantics.
+#include <cstddef>
+
+#include "mpf_arith.cuh"
+
+using namespace mpfk::arith;
+
+extern "C" {
+
+int hst_binop_batch(int W, int op, std::size_t count, const double* x, const double* y,
+                    double* r) {
+  for (std::size_t i = 0; i < count; ++i) {
+    const double* a = x + i * W;
+    const double* b = y + i * W;
+    double* c = r + i * W;
+    switch (W * 2 + op) {
+      case 4: mp_add<2>(a, b, c); break;
+      case 5: mp_mul<2>(a, b, c); break;
+      case 6: mp_add<3>(a, b, c); break;
+      case 7: mp_mul<3>(a, b, c); break;
+      case 8: mp_add<4>(a, b, c); break;
+      case 9: mp_mul<4>(a, b, c); break;
+      default: return 1;
+    }
+  }
+  return 0;
+}
+
+void hst_renorm5_batch(std::size_t count, const double* c, double* r) {
+  for (std::size_t i = 0; i < count; ++i) {
+    const double* x = c + 5 * i;
+    double* o = r + 4 * i;
+    renorm5(x[0], x[1], x[2], x[3], x[4], o[0], o[1], o[2], o[3]);
+  }
+}
+
+void hst_vseb23_batch(std::size_t count, const double* e, double* out) {
+  for (std::size_t i = 0; i < count; ++i) vseb_2_3(e[3 * i], e[3 * i + 1], e[3 * i + 2], out[2 * i], out[2 * i + 1]);
+}
+
+// the GEMM's per-element order (mul first, then add(C, p) ascending k) on the
+// host with the product arithmetic
+void hst_gemm(int W, std::size_t m, std::size_t K, std::size_t n, const double* A, std::size_t lda,
+              const double* B, std::size_t ldb, double* C, std::size_t ldc) {
+  const std::size_t pa = m * lda, pb = K * ldb, pc = m * ldc;
+  for (std::size_t i = 0; i < m; ++i)
+    for (std::size_t j = 0; j < n; ++j) {
+      double acc[4] = {0, 0, 0, 0};
+      for (std::size_t k = 0; k < K; ++k) {
+        double a[4], b[4], p[4];
+        for (int w = 0; w < W; ++w) a[w] = A[w * pa + i * lda + k], b[w] = B[w * pb + k * ldb + j];
+        if (W == 2) mp_mul<2>(a, b, p);
+        else if (W == 3) mp_mul<3>(a, b, p);
+        else mp_mul<4>(a, b, p);
+        if (k == 0) {
+          for (int w = 0; w < W; ++w) acc[w] = p[w];
+        } else if (W == 2) mp_add<2>(acc, p, acc);
+        else if (W == 3) mp_add<3>(acc, p, acc);
+        else mp_add<4>(acc, p, acc);
+      }
+      for (int w = 0; w < W; ++w) C[w * pc + i * ldc + j] = acc[w];
+    }
+}
+
+}  // extern "C"
