@@ -69,16 +69,6 @@ def dist_env():
     return ws, rank, local
 
 
-def shard_rows(m, world, rank, align=64):
-    """Contiguous row span of `rank` (the reference's worker partition,
-    linalg.hpp:413-421, in 64-row blocks)."""
-    nblocks = (m + align - 1) // align
-    per = (nblocks + world - 1) // world
-    r0 = min(m, rank * per * align)
-    r1 = min(m, (rank + 1) * per * align)
-    return r0, r1
-
-
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
 
@@ -225,6 +215,7 @@ def run_mpfk(args, ws, rank, local):
     import torch.distributed as dist
 
     import paper_2101_06584_b200 as P
+    from paper_2101_06584_b200.dist import shard_rows, sharded_gemm_step
 
     W, n, wide = WORKLOADS[args.workload]
     m = k = n
@@ -252,13 +243,16 @@ def run_mpfk(args, ws, rank, local):
     launches = [0]
 
     def step():
-        if ws > 1:
-            dist.broadcast(dB, src=0)
         ev_mid = torch.cuda.Event(enable_timing=True)
-        ev_mid.record(stream)
-        if rows:
-            launches[0] += P.gemm_device(W, rows, n, k, dA.data_ptr(), ld, rows * ld, dB.data_ptr(), ld, k * ld,
-                                         dC.data_ptr(), ld, rows * ld, stream.cuda_stream)
+
+        def gemm(W_, dA_, dB_, dC_, rows_, n_, k_, ld_):
+            ev_mid.record(stream)  # after the B broadcast
+            return P.gemm_device(W_, rows_, n_, k_, dA_.data_ptr(), ld_, rows_ * ld_, dB_.data_ptr(), ld_,
+                                 k_ * ld_, dC_.data_ptr(), ld_, rows_ * ld_, stream.cuda_stream)
+
+        launches[0] += sharded_gemm_step(W, dA, dB, dC, rows, n, k, ld, gemm=gemm)
+        if not rows:
+            ev_mid.record(stream)
         return ev_mid
 
     for _ in range(args.warmup):
