@@ -53,16 +53,18 @@ def sharded_gemm_step(W: int, dA, dB, dC, rows: int, n: int, k: int, ld: int, *,
     return gemm(W, dA, dB, dC, rows, n, k, ld)
 
 
-def gather_c(dC_shard, m: int, world: int, group=None):
+def gather_c(dC_shard, m: int, world: int, group=None, align: int = 64):
     """Assemble the replicated (W, m, ld) C from the row shards
-    (all-gather); shards are padded to the common span length."""
+    (all-gather); shards are padded to the common span length.  `align`
+    must be the one the shards were cut with (shard_rows)."""
     import torch
     import torch.distributed as dist
     W, rows, ld = dC_shard.shape
-    per = shard_rows(m, world, 0)[1]
+    per = max(1, shard_rows(m, world, 0, align)[1])
     buf = torch.zeros((W, per, ld), dtype=dC_shard.dtype, device=dC_shard.device)
     buf[:, :rows] = dC_shard[:, :rows]
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf.contiguous(), group=group)
-    out = torch.cat([p for p in parts], dim=1)[:, :m]
+    spans = [shard_rows(m, world, r, align) for r in range(world)]
+    out = torch.cat([p[:, : r1 - r0] for p, (r0, r1) in zip(parts, spans)], dim=1)
     return out.contiguous()

@@ -1,0 +1,134 @@
+"""The product's device arithmetic (csrc/mpf_arith.cuh), compiled for the host
+(tests/_build/libarith_host.so, -ffp-contract=off), against the reference
+build on the CPU: the branch-free renorm5/vseb restatements and every width
+kernel must be bit-identical on random, wide-range and special inputs.  The
+device build uses __dadd_rn & co. with the same IEEE semantics; the GPU
+tests (test_gemm_gpu.py) close that last step on the B200.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from tests.helpers import mismatches, random_signed, special_matrix
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "_build", "libarith_host.so")
+
+pytestmark = [pytest.mark.skipif(not os.path.exists(SO), reason="host arith shim not built"),
+              pytest.mark.skipif(not O.ref_available(), reason="reference build absent")]
+
+
+@pytest.fixture(scope="module")
+def H():
+    L = C.CDLL(SO)
+    L.hst_binop_batch.argtypes = [C.c_int, C.c_int, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.hst_renorm5_batch.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p]
+    L.hst_vseb23_batch.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p]
+    L.hst_gemm.argtypes = [C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_size_t, C.c_void_p,
+                           C.c_size_t, C.c_void_p, C.c_size_t]
+    return L
+
+
+def _pairs(W, count, seed):
+    st = (C.c_uint64 * 1)(seed)
+    x = np.zeros((count, W))
+    for i in range(count):
+        O.ref().ref_random_normalized(W, C.cast(st, C.c_void_p), 1, x[i].ctypes.data)
+    return x
+
+
+def _special_values(W, count, seed):
+    """mixtures of +-0, integers, powers of two and normalized values per
+    component slot -- including non-normalized combinations that drive every
+    renorm5 path."""
+    rng = np.random.default_rng(seed)
+    pool = np.array([0.0, -0.0, 1.0, -1.0, 2.0, 0.5, 3.0, -3.0, 2.0 ** -53, -2.0 ** -53, 2.0 ** -106,
+                     2.0 ** -159, 2.0 ** 30, 1.0 + 2.0 ** -52, 7.0, -2.0 ** -1074])
+    x = rng.choice(pool, size=(count, W))
+    norm = _pairs(W, count, seed + 1)
+    pick = rng.integers(0, 3, size=(count, 1))
+    return np.where(pick == 0, norm, x)
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+@pytest.mark.parametrize("op", ["add", "mul"])
+def test_width_kernels_random(H, W, op):
+    n = 40000
+    x = _pairs(W, n, 10 + W)
+    y = _pairs(W, n, 20 + W) * np.ldexp(1.0, np.random.default_rng(W).integers(-80, 80, (n, 1)))
+    y[::7] = -x[::7] * (1 + 2.0 ** -40)  # near cancellation
+    r = np.empty_like(x)
+    H.hst_binop_batch(W, {"add": 0, "mul": 1}[op], n, x.ctypes.data, y.ctypes.data, r.ctypes.data)
+    want = O.ref_binop_batch(W, op, x, y)
+    assert not (r.view(np.uint64) != want.view(np.uint64)).any()
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+@pytest.mark.parametrize("op", ["add", "mul"])
+def test_width_kernels_special(H, W, op):
+    n = 40000
+    x = _special_values(W, n, 30 + W)
+    y = _special_values(W, n, 40 + W)
+    r = np.empty_like(x)
+    H.hst_binop_batch(W, {"add": 0, "mul": 1}[op], n, x.ctypes.data, y.ctypes.data, r.ctypes.data)
+    want = O.ref_binop_batch(W, op, x, y)
+    bad = (r.view(np.uint64) != want.view(np.uint64)).any(axis=1)
+    assert not bad.any(), (x[bad][:3], y[bad][:3], r[bad][:3], want[bad][:3])
+
+
+def test_renorm5_all_paths(H):
+    """Branch-free fast path + verbatim fallback vs eft.hpp:241-288 on inputs
+    hitting paths A-D and the zero corners."""
+    rng = np.random.default_rng(5)
+    n = 100000
+    c = np.zeros((n, 5))
+    c[:, 0] = 1.0 + rng.random(n)
+    for i in range(1, 5):
+        c[:, i] = (rng.random(n) * 2 - 1) * np.ldexp(2.0, -53 * i)
+    # zero out random subsets of tail terms, and plant exact cancellations
+    mask = rng.random((n, 5)) < 0.3
+    mask[:, 0] = False
+    c[mask] = 0.0
+    c[::11, 2] = -c[::11, 1]
+    c[::13, 4] = -0.0
+    out = np.zeros((n, 4))
+    H.hst_renorm5_batch(n, c.ctypes.data, out.ctypes.data)
+    want = np.zeros((n, 4))
+    for i in range(n):
+        O.ref().ref_renorm5(c[i].ctypes.data, want[i].ctypes.data)
+    assert not (out.view(np.uint64) != want.view(np.uint64)).any()
+
+
+def test_vseb_2_3(H):
+    """vseb with k = 2, n = 3 (td_mul's use, mpf.hpp:162) vs eft.hpp:205-225."""
+    rng = np.random.default_rng(6)
+    n = 60000
+    e = np.zeros((n, 3))
+    e[:, 0] = rng.random(n) * 2 - 1
+    e[:, 1] = (rng.random(n) * 2 - 1) * 2.0 ** -53
+    e[:, 2] = (rng.random(n) * 2 - 1) * 2.0 ** -106
+    z = rng.random((n, 3)) < 0.25
+    e[z] = 0.0
+    e[::9, 2] = -0.0
+    e[::5, 1] = 0.0
+    out = np.zeros((n, 2))
+    H.hst_vseb23_batch(n, e.ctypes.data, out.ctypes.data)
+    want = np.zeros((n, 2))
+    for i in range(n):
+        assert O.ref().ref_vseb(e[i].ctypes.data, 3, want[i].ctypes.data, 2) == 0
+    assert not (out.view(np.uint64) != want.view(np.uint64)).any()
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+def test_gemm_order_on_host(H, W):
+    """The kernel's per-element order (mul, then add(C, p) ascending k) with
+    the product arithmetic == the reference GEMM."""
+    for (m, k, n), gen in [((17, 23, 19), random_signed), ((20, 20, 20), special_matrix)]:
+        A = gen(W, m, k, 60 + m)
+        B = gen(W, k, n, 70 + n)
+        Cm = O.planes(W, m, n)
+        H.hst_gemm(W, m, k, n, A.ctypes.data, A.shape[2], B.ctypes.data, B.shape[2], Cm.ctypes.data, Cm.shape[2])
+        assert mismatches(Cm, O.ref_gemm(A, B, k, n)) == 0

@@ -1,0 +1,83 @@
+"""The N > 1 path on the CPU with the gloo backend, world_size 2 (the GPU box
+has one GPU): the product's row partition (paper_2101_06584_b200.dist) plus
+the B replication and the C all-gather, with the per-rank GEMM done by the
+oracle through the driver's compute hook.  The assembled C must be
+bit-identical to the single-rank GEMM, exactly as the reference's worker
+partition is (linalg.hpp:399-433, acceptance.cpp:363-395)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2101_06584_b200.dist import gather_c, shard_rows, sharded_gemm_step
+
+
+def test_shard_rows_partition():
+    for m in (1, 63, 64, 65, 1000, 8192):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_rows(m, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0 and a0 <= a1
+            for r0, r1 in spans:
+                assert r0 % 64 == 0 or r0 == r1 == m
+    with pytest.raises(ValueError):
+        shard_rows(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, W, m, k, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle as O
+        ld = (n + 3) & ~3
+        A = O.orc_fill_baseline(W, m, k, 1, wide=W > 2)
+        r0, r1 = shard_rows(m, world, rank, align=8)
+        rows = r1 - r0
+        dA = torch.from_numpy(np.ascontiguousarray(A[:, r0:r1]))
+        dB = torch.zeros((W, k, ld), dtype=torch.float64)
+        if rank == 0:
+            dB.copy_(torch.from_numpy(O.orc_fill_baseline(W, k, n, 2, wide=W > 2)))
+        dC = torch.zeros((W, max(rows, 1), ld), dtype=torch.float64)
+
+        def oracle_gemm(W_, dA_, dB_, dC_, rows_, n_, k_, ld_):
+            Cs = O.orc_gemm(dA_.numpy(), dB_.numpy(), k_, n_)
+            dC_[:, :rows_] = torch.from_numpy(Cs)
+            return 1
+
+        launches = sharded_gemm_step(W, dA, dB, dC, rows, n, k, ld, gemm=oracle_gemm)
+        Cfull = gather_c(dC[:, :rows], m, world, align=8)
+        if rank == 0:
+            want = O.orc_gemm(A, O.orc_fill_baseline(W, k, n, 2, wide=W > 2), k, n)
+            same = np.array_equal(Cfull.numpy().view(np.uint64), want.view(np.uint64))
+            q.put((same, launches))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("W,m,k,n", [(2, 37, 21, 19), (3, 16, 9, 10), (4, 20, 7, 6)])
+def test_two_rank_gloo_row_shards_bit_identical(W, m, k, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, W, m, k, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    same, launches = q.get(timeout=10)
+    assert same and launches == 1
