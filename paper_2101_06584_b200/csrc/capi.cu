@@ -202,8 +202,9 @@ void launch_cfg(const kern::GemmArgs& g, cudaStream_t s) {
        "cudaFuncSetAttribute");
     configured_dev = dev;
   }
-  dim3 grid((g.N + Cfg::BN - 1) / Cfg::BN, (g.M + Cfg::BM - 1) / Cfg::BM);
-  kern::mpgemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g);
+  const long long tiles = (long long)((g.N + Cfg::BN - 1) / Cfg::BN) * ((g.M + Cfg::BM - 1) / Cfg::BM);
+  if (tiles > 0x7fffffffLL) fail(MPFK_EINVAL, "mpfk: too many tiles");
+  kern::mpgemm_kernel<Cfg><<<(unsigned)tiles, Cfg::THREADS, Cfg::SMEM, s>>>(g);
   ck(cudaGetLastError(), "GEMM kernel launch");
 }
 

@@ -47,10 +47,15 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1>
+// GROUP_M: tiles are visited in column-major order within bands of GROUP_M
+// tile rows, so the CTAs resident at one time cover a near-square block of C
+// and share their A and B panels in L2 instead of streaming all of B per
+// tile row.
+template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
+          int GROUP_M_ = 16, int MINB_ = 1>
 struct TileCfg {
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
-  static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_;
+  static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
   static constexpr int TX = BN / TN;  // threads along N
   static constexpr int TY = BM / TM;  // threads along M
   static constexpr int THREADS = TX * TY;
@@ -90,8 +95,24 @@ __device__ __forceinline__ void load_tile(double* As, double* Bs, const GemmArgs
   }
 }
 
+// linear CTA index -> (tile row, tile col) with GROUP_M-row bands
+template <int GROUP_M>
+__device__ __forceinline__ void tile_coords(int lin, int tiles_m, int tiles_n, int& tm, int& tn) {
+  if (GROUP_M <= 1) {
+    tm = lin / tiles_n;
+    tn = lin % tiles_n;
+    return;
+  }
+  const int band = lin / (GROUP_M * tiles_n);
+  const int first = band * GROUP_M;
+  const int rows = min(GROUP_M, tiles_m - first);
+  const int local = lin - band * GROUP_M * tiles_n;
+  tm = first + local % rows;
+  tn = local / rows;
+}
+
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS)
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     mpgemm_kernel(const GemmArgs g) {
   constexpr int W = Cfg::W, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, TX = Cfg::TX, TY = Cfg::TY;
@@ -101,7 +122,9 @@ __global__ void __launch_bounds__(Cfg::THREADS)
   double* Bs0 = smem + STAGES * Cfg::A_STAGE;
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  int tile_m, tile_n;
+  tile_coords<Cfg::GROUP_M>(blockIdx.x, (g.M + BM - 1) / BM, (g.N + BN - 1) / BN, tile_m, tile_n);
+  const int m0 = tile_m * BM, n0 = tile_n * BN;
   const int ktiles = (g.K + BK - 1) / BK;
 
   double acc[TM][TN][W];

@@ -17,12 +17,13 @@
 
 #include <stdint.h>
 
+#include <cmath>
+#include <cstring>
+
 #if defined(__CUDACC__)
 #define MPFK_HD __host__ __device__ __forceinline__
 #else
 #define MPFK_HD inline __attribute__((always_inline))
-#include <cmath>
-#include <cstring>
 #endif
 
 namespace mpfk {
@@ -259,7 +260,40 @@ MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
 }
 
 // td_add_q, mpf.hpp:135-142: zero-extend with +0, quad add, truncate.
+//
+// qd_add on (x0,x1,x2,+0) + (y0,y1,y2,+0) with the constant lane folded.
+// Every fold is a bitwise identity of the reference sequence for finite
+// operands (the EFT domain, eft.hpp:44-45):
+//  * two_sum(+0, +0) = (+0, +0): s = +0, v = +0, e = (+0 - +0) + (+0 - +0).
+//  * two_sum(+0, b) (first step of three_sum2(s3 = +0, t0, t2)):
+//      s = +0 + b, v = s - +0 = s, s - v = +0, so
+//      e = (+0 - +0) + (b - s) = +0 + (b - s), where b - s is +0 for b != -0
+//      and -0 - +0 = -0 for b = -0; +0 + (+-0) = +0.  Hence (s, e) =
+//      (+0 + b, +0): one add instead of six.
+//  * three_sum2's error t.e + u.e = +0 + u.e stays one add (it maps -0 to +0).
+//  * t0 + t3 with t3 = +0 stays (same reason).
+// 11 of td_add_q's 85 FP64 operations disappear; results are unchanged
+// (tests/test_arith_host.py sweeps signed zeros against the reference).
 MPFK_HD void td_add_q(const double* x, const double* y, double* r) {
+  double s0, t0, s1, t1, s2, t2;
+  two_sum(x[0], y[0], s0, t0);
+  two_sum(x[1], y[1], s1, t1);
+  two_sum(x[2], y[2], s2, t2);
+  two_sum(s1, t0, s1, t0);
+  three_sum(s2, t0, t1, s2, t0, t1);
+  // three_sum2(+0, t0, t2), eft.hpp:95-99, with the folds above
+  const double ts = add(0.0, t0);
+  double s3, ue;
+  two_sum(t2, ts, s3, ue);
+  t0 = add(0.0, ue);
+  t0 = add(add(t0, t1), 0.0);
+  double r3;
+  renorm5(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3);
+}
+
+// td_add_q without the folds (the literal zero-extend + qd_add); kept for
+// the cross-check in tests (arith_host.cpp) and as documentation.
+MPFK_HD void td_add_q_unfolded(const double* x, const double* y, double* r) {
   const double xx[4] = {x[0], x[1], x[2], 0.0};
   const double yy[4] = {y[0], y[1], y[2], 0.0};
   qd_add<true>(xx, yy, r);

@@ -31,6 +31,11 @@ int hst_binop_batch(int W, int op, std::size_t count, const double* x, const dou
   return 0;
 }
 
+// the literal zero-extend + qd_add form of td_add_q (no folds)
+void hst_td_add_unfolded_batch(std::size_t count, const double* x, const double* y, double* r) {
+  for (std::size_t i = 0; i < count; ++i) td_add_q_unfolded(x + 3 * i, y + 3 * i, r + 3 * i);
+}
+
 void hst_renorm5_batch(std::size_t count, const double* c, double* r) {
   for (std::size_t i = 0; i < count; ++i) {
     const double* x = c + 5 * i;

@@ -79,6 +79,23 @@ def test_width_kernels_special(H, W, op):
     assert not bad.any(), (x[bad][:3], y[bad][:3], r[bad][:3], want[bad][:3])
 
 
+def test_td_add_folds_are_identities(H):
+    """td_add_q with the constant-lane folds == the literal zero-extend +
+    qd_add sequence == the reference, on signed-zero-heavy inputs."""
+    H.hst_td_add_unfolded_batch.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
+    n = 60000
+    x = _special_values(3, n, 91)
+    y = _special_values(3, n, 92)
+    y[::3] = -x[::3]
+    folded = np.empty_like(x)
+    unfolded = np.empty_like(x)
+    H.hst_binop_batch(3, 0, n, x.ctypes.data, y.ctypes.data, folded.ctypes.data)
+    H.hst_td_add_unfolded_batch(n, x.ctypes.data, y.ctypes.data, unfolded.ctypes.data)
+    want = O.ref_binop_batch(3, "add", x, y)
+    assert not (folded.view(np.uint64) != unfolded.view(np.uint64)).any()
+    assert not (folded.view(np.uint64) != want.view(np.uint64)).any()
+
+
 def test_renorm5_all_paths(H):
     """Branch-free fast path + verbatim fallback vs eft.hpp:241-288 on inputs
     hitting paths A-D and the zero corners."""
