@@ -187,12 +187,16 @@ void grow(double*& p, size_t& cap, size_t bytes) {
 // ---------------------------------------------------------------------------
 // kernel dispatch per width
 // ---------------------------------------------------------------------------
-using Cfg2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 2>;
-using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1>;
-using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1>;
+// Tile configurations chosen by the sweep in scripts/tune.py over
+// csrc/tune.cu (profiles/r01_tune.log): the occupancy floor (MINB) matters
+// most -- it caps registers so 2-3 CTAs share each SM's FP64 pipe.
+using Cfg2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 2, 16, 2>;     // DD, large problems
+using Cfg2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 2, 16, 4>;    // DD, few waves
+using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 3>;     // TD
+using Cfg4 = kern::TileCfg<4, 16, 32, 16, 1, 2, 2, 1, 16, 3>;     // QD
 
 template <class Cfg>
-void launch_cfg(const kern::GemmArgs& g, cudaStream_t s) {
+void configure_once() {
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -202,7 +206,31 @@ void launch_cfg(const kern::GemmArgs& g, cudaStream_t s) {
        "cudaFuncSetAttribute");
     configured_dev = dev;
   }
-  const long long tiles = (long long)((g.N + Cfg::BN - 1) / Cfg::BN) * ((g.M + Cfg::BM - 1) / Cfg::BM);
+}
+
+template <class Cfg>
+long long tiles_of(const kern::GemmArgs& g) {
+  return (long long)((g.N + Cfg::BN - 1) / Cfg::BN) * ((g.M + Cfg::BM - 1) / Cfg::BM);
+}
+
+// Expected fraction of FP64 peak: steady-state efficiency of the tile shape
+// (measured by the sweep) times the per-SM balance of the tile count -- the
+// FP64 pipe is shared by all CTAs resident on an SM, so what quantises is
+// tiles per SM (tiles / SMs vs its ceiling), e.g. DD n=1024: 256 64x64 tiles
+// -> 1.73 per SM (0.86), 1024 32x32 tiles -> 6.92 per SM (0.99).
+template <class Cfg>
+double predicted_eff(const kern::GemmArgs& g, double steady) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const double per_sm = double(tiles_of<Cfg>(g)) / std::max(sms, 1);
+  return steady * per_sm / std::ceil(per_sm);
+}
+
+template <class Cfg>
+void launch_cfg(const kern::GemmArgs& g, cudaStream_t s) {
+  configure_once<Cfg>();
+  const long long tiles = tiles_of<Cfg>(g);
   if (tiles > 0x7fffffffLL) fail(MPFK_EINVAL, "mpfk: too many tiles");
   kern::mpgemm_kernel<Cfg><<<(unsigned)tiles, Cfg::THREADS, Cfg::SMEM, s>>>(g);
   ck(cudaGetLastError(), "GEMM kernel launch");
@@ -237,7 +265,12 @@ int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uin
   g.pa = (long long)pa, g.pb = (long long)pb, g.pc = (long long)pc;
   g.M = (int)m, g.N = (int)n, g.K = (int)k;
   switch (W) {
-    case 2: launch_cfg<Cfg2>(g, s); break;
+    case 2:
+      if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
+        launch_cfg<Cfg2s>(g, s);
+      else
+        launch_cfg<Cfg2>(g, s);
+      break;
     case 3: launch_cfg<Cfg3>(g, s); break;
     case 4: launch_cfg<Cfg4>(g, s); break;
     default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
