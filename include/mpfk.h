@@ -58,12 +58,14 @@ typedef struct mpfk_mat {
   uint64_t plane_stride; /* doubles between planes; 0 means rows * stride */
 } mpfk_mat;
 
-/* Timings of the last host-buffer GEMM on this thread (device clocks, ms). */
+/* Timings of the last host-buffer GEMM on this thread (device clocks, ms,
+ * max over GPUs).  Row chunks are pipelined: uploads of chunk c+1 and the
+ * download of chunk c-1 overlap the GEMM of chunk c, so the parts overlap. */
 typedef struct mpfk_stats {
-  double h2d_ms;    /* host->device copies of A shards and B slices */
+  double h2d_ms;    /* span of the host->device copies (B slice, A chunks) */
   double bcast_ms;  /* B replication over NVLink (peer all-gather), G > 1 */
-  double kernel_ms; /* max over GPUs of the GEMM kernel */
-  double d2h_ms;    /* device->host copy of the C shards */
+  double kernel_ms; /* span of the GEMM launches (first chunk to last) */
+  double d2h_ms;    /* exposed device->host tail after the last GEMM */
   double total_ms;  /* whole call, host wall clock */
   uint64_t h2d_bytes, d2h_bytes, peer_bytes;
   int n_gpus;
@@ -121,6 +123,24 @@ int mpfk_gemm_device(int width, uint64_t m, uint64_t n, uint64_t k, const double
                      int *launches);
 
 /* ---- elementwise width kernels (mpf::add/mul<W>, mpf.hpp:341-353) ------- */
+
+/* EwOp, linalg.hpp:623 */
+enum mpfk_ew_op { MPFK_EW_ADD = 0, MPFK_EW_MUL = 1, MPFK_EW_ADD_MERGE = 2 };
+
+/* linalg::ew_apply_into(out, a, b, op, variant), linalg.hpp:647-684:
+ * out = op(a, b) cell by cell on the GPU (add/mul: the width's library
+ * defaults, mpf.hpp:242-260; add_merge: td_add_merge, mpf.hpp:125-131, W = 3
+ * only).  Errors "ew: shape mismatch" / "ew: add_merge is a triple-width
+ * operation" (linalg.hpp:650-653).  SIMD variants leave out's pads +0, NORMAL
+ * leaves them untouched, as in the reference.  Counts adds (add, add_merge)
+ * or muls (mul) += rows*cols (linalg.hpp:682-683).  Synchronous. */
+int mpfk_ew_apply_into(int width, int op, mpfk_mat *out, const mpfk_mat *a, const mpfk_mat *b,
+                       int variant);
+/* device-resident form on the current device / `stream`, asynchronous; only
+ * the rows x cols cells of out are written; 16-byte aligned, even strides. */
+int mpfk_ew_device(int width, int op, uint64_t rows, uint64_t cols, double *out, uint64_t ldo,
+                   uint64_t o_plane, const double *a, uint64_t lda, uint64_t a_plane,
+                   const double *b, uint64_t ldb, uint64_t b_plane, void *stream, int *launches);
 
 /* r[i] = op(x[i], y[i]) for `count` values stored AoS (W doubles each) in
  * host memory, computed on the GPU.  op: 0 = add, 1 = mul (library

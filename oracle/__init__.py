@@ -81,6 +81,8 @@ def ref():
         L.ref_op_counts.argtypes = [_D, _D]
         L.ref_random_normalized.argtypes = [C.c_int, _D, C.c_int, _D]
         L.ref_hardware_concurrency.restype = C.c_uint
+        L.ref_ew.argtypes = [C.c_int, C.c_int, C.c_int, _S, _S, _D, _S, _D, _S, _D, _S]
+        L.ref_td_add_merge_batch.argtypes = [_S, _D, _D, _D]
         _ref = L
     return _ref
 
@@ -171,3 +173,16 @@ def orc_binop_batch(W, op, x, y):
     for i in range(x.shape[0]):
         f(W, x[i].ctypes.data, y[i].ctypes.data, r[i].ctypes.data)
     return r
+
+
+def ref_ew(W, op, a, b, cols, variant=0):
+    """linalg::ew_apply_into on plane arrays (W, rows, ld); op 'add'|'mul'|'add_merge'."""
+    _, rows, lda = a.shape
+    out = np.zeros_like(a)
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    rc = ref().ref_ew(W, {"add": 0, "mul": 1, "add_merge": 2}[op], variant, rows, cols, _p(a), lda, _p(b),
+                      b.shape[2], _p(out), out.shape[2])
+    if rc:
+        raise ValueError(ref().ref_last_error().decode())
+    return out

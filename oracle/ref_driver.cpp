@@ -115,6 +115,19 @@ void gen_paper_w(std::size_t n, double* A, double* B, std::size_t ld) {
 }
 
 template <int W>
+int ew_w(int op, int variant, std::size_t rows, std::size_t cols, const double* a, std::size_t lda,
+         const double* b, std::size_t ldb, double* out, std::size_t ldo) {
+  return guarded([&] {
+    const auto x = load<W>(a, rows, cols, lda);
+    const auto y = load<W>(b, rows, cols, ldb);
+    linalg::MPMatrix<W> o(rows, cols);
+    linalg::ew_apply_into(o, x, y, static_cast<linalg::EwOp>(op),
+                          static_cast<linalg::KernelVariant>(variant));
+    store<W>(o, out, ldo);
+  });
+}
+
+template <int W>
 void binop_w(int op, const double* x, const double* y, double* r) {
   mpf::MultiDouble<W> a, b;
   for (int w = 0; w < W; ++w) a.c[w] = x[w], b.c[w] = y[w];
@@ -193,6 +206,25 @@ int ref_binop(int W, int op, const double* x, const double* y, double* r) {
   else if (W == 4) binop_w<4>(op, x, y, r);
   else return 1;
   return 0;
+}
+
+// linalg::ew_apply_into (linalg.hpp:647-684); op: 0 add, 1 mul, 2 add_merge
+int ref_ew(int W, int op, int variant, std::size_t rows, std::size_t cols, const double* a,
+           std::size_t lda, const double* b, std::size_t ldb, double* out, std::size_t ldo) {
+  if (W == 2) return ew_w<2>(op, variant, rows, cols, a, lda, b, ldb, out, ldo);
+  if (W == 3) return ew_w<3>(op, variant, rows, cols, a, lda, b, ldb, out, ldo);
+  if (W == 4) return ew_w<4>(op, variant, rows, cols, a, lda, b, ldb, out, ldo);
+  return 1;
+}
+
+// td_add_merge over a batch (mpf.hpp:305-309)
+void ref_td_add_merge_batch(std::size_t count, const double* x, const double* y, double* r) {
+  for (std::size_t i = 0; i < count; ++i) {
+    const mpf::Double3 a{{x[3 * i], x[3 * i + 1], x[3 * i + 2]}};
+    const mpf::Double3 b{{y[3 * i], y[3 * i + 1], y[3 * i + 2]}};
+    const auto c = mpf::td_add_merge(a, b);
+    for (int w = 0; w < 3; ++w) r[3 * i + w] = c.c[w];
+  }
 }
 
 // Batched forms for million-sample sweeps (one call, no per-call overhead).

@@ -2,12 +2,18 @@
 sm_100a).  The compute lives in libmpfk.so (csrc/); this package is the
 Python mirror of the reference's mpfkit::linalg API over its C ABI."""
 from .linalg import (  # noqa: F401
+    EwOp,
     KernelVariant,
     MPMatrix,
     OpCounts,
     binop_batch,
     bits_equal,
     device_count,
+    ew_add,
+    ew_add_merge,
+    ew_apply_into,
+    ew_device,
+    ew_mul,
     fill_baseline,
     format_eps,
     fp64_peak,

@@ -66,6 +66,10 @@ _SIGS = {
     "mpfk_last_stats": (C.c_int, [C.POINTER(MpfkStats)]),
     "mpfk_gemm_device": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                    _U64, _P, C.POINTER(C.c_int)]),
+    "mpfk_ew_apply_into": (C.c_int, [C.c_int, C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat),
+                                     C.POINTER(MpfkMat), C.c_int]),
+    "mpfk_ew_device": (C.c_int, [C.c_int, C.c_int, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64,
+                                 _P, C.POINTER(C.c_int)]),
     "mpfk_binop_batch": (C.c_int, [C.c_int, C.c_int, _U64, _P, _P, _P]),
     "mpfk_op_counters_reset": (None, []),
     "mpfk_op_counters_read": (None, [C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)]),

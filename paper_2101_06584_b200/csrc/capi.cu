@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/mpfk.h"
+#include "ew_kernel.cuh"
 #include "gemm_kernel.cuh"
 #include "mpf_arith.cuh"
 
@@ -95,11 +96,17 @@ __global__ void selftest_kernel(const double* in, int* ok) {
   *ok = (rn ? 1 : 0) | (fused ? 2 : 0);
 }
 
+constexpr int kMaxChunks = 8;
+
 struct Device {
   int id = -1;
   bool ready = false;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // compute
+  cudaStream_t up = nullptr;      // host->device copies
+  cudaStream_t down = nullptr;    // device->host copies
   cudaEvent_t ev[6] = {};
+  cudaEvent_t evA[kMaxChunks] = {};  // A row chunk c resident
+  cudaEvent_t evC[kMaxChunks] = {};  // C row chunk c computed
   // grow-only operand buffers for the host-buffer path
   double* dA = nullptr;
   double* dB = nullptr;
@@ -169,7 +176,11 @@ void ensure_devices(int n) {
     ck(cudaSetDevice(d), "cudaSetDevice");
     run_selftest_current();
     ck(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&D.up, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&D.down, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : D.ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    for (auto& e : D.evA) ck(cudaEventCreate(&e), "cudaEventCreate");
+    for (auto& e : D.evC) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     D.ready = true;
   }
   cudaSetDevice(prev);
@@ -276,6 +287,42 @@ int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uin
     default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
   }
   return 1;
+}
+
+// Enqueue out = op(a, b) elementwise on the current device.
+int enqueue_ew(int W, int op, uint64_t rows, uint64_t cols, double* out, uint64_t ldo, uint64_t po,
+               const double* a, uint64_t lda, uint64_t pa, const double* b, uint64_t ldb,
+               uint64_t pb, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return 0;
+  if (rows > 0x7fffffffULL || cols > 0x7fffffffULL) fail(MPFK_EINVAL, "mpfk: dimension exceeds 2^31-1");
+  kern::EwArgs g;
+  g.out = out, g.a = a, g.b = b;
+  g.ldo = (long long)ldo, g.lda = (long long)lda, g.ldb = (long long)ldb;
+  g.po = (long long)po, g.pa = (long long)pa, g.pb = (long long)pb;
+  g.rows = (int)rows, g.cols = (int)cols;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t work = rows * ((cols + 1) / 2);
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, (uint64_t)sms * 8));
+#define MPFK_EW(WW, OO) kern::ew_kernel<WW, OO><<<blocks, 256, 0, s>>>(g)
+  switch (W * 4 + op) {
+    case 8: MPFK_EW(2, kern::EW_ADD); break;
+    case 9: MPFK_EW(2, kern::EW_MUL); break;
+    case 12: MPFK_EW(3, kern::EW_ADD); break;
+    case 13: MPFK_EW(3, kern::EW_MUL); break;
+    case 14: MPFK_EW(3, kern::EW_ADD_MERGE); break;
+    case 16: MPFK_EW(4, kern::EW_ADD); break;
+    case 17: MPFK_EW(4, kern::EW_MUL); break;
+    default: fail(MPFK_EINVAL, "ew: add_merge is a triple-width operation");
+  }
+#undef MPFK_EW
+  ck(cudaGetLastError(), "ew kernel launch");
+  return 1;
+}
+
+void count_ew(int op, uint64_t rows, uint64_t cols) {  // linalg.hpp:682-683
+  (op == kern::EW_MUL ? g_muls : g_adds).fetch_add(rows * cols, std::memory_order_relaxed);
 }
 
 void check_width(int W) {
@@ -388,7 +435,19 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   std::vector<Fail> fails(G);
   std::vector<int> failed(G, 0);
 
-  auto phase1 = [&](int g) {  // allocate + upload A shard and B slice
+  // Row chunks of each shard are pipelined over three streams: H2D of chunk
+  // c+1 (copy engine) and D2H of chunk c-1 (second copy engine) overlap the
+  // GEMM of chunk c.  Rows of C are independent, so chunking cannot change a
+  // bit.  A chunk is sized to keep >= 4 tiles per SM per launch.
+  auto chunks_of = [&](uint64_t rows) {
+    const double tiles_per_row = double(n) / (64.0 * 64.0);
+    const uint64_t min_rows = (uint64_t)std::ceil(148.0 * 4.0 / std::max(tiles_per_row, 1e-9));
+    uint64_t nc = std::max<uint64_t>(1, std::min<uint64_t>(kMaxChunks, rows / std::max<uint64_t>(min_rows, 1)));
+    const uint64_t crows = ((rows + nc - 1) / nc + 63) / 64 * 64;
+    return std::make_pair((rows + crows - 1) / std::max<uint64_t>(crows, 1), crows);
+  };
+  std::vector<int> nchunks(G, 0);
+  auto phase1 = [&](int g) {  // allocate; upload the B slice, then A row chunks
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -396,25 +455,33 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(rows * lda, 1));
     grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
     grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(rows * ldc, 1));
-    ck(cudaEventRecord(D.ev[0], D.stream), "event");
-    for (int w = 0; w < W; ++w) {
-      if (rows && K)
-        ck(cudaMemcpy2DAsync(D.dA + w * rows * lda, lda * 8, A->base + w * pa_h + s.r0 * A->stride,
-                             A->stride * 8, K * 8, rows, cudaMemcpyHostToDevice, D.stream),
-           "H2D A");
+    ck(cudaEventRecord(D.ev[0], D.up), "event");
+    for (int w = 0; w < W; ++w)
       if (s.b1 > s.b0 && n)
         ck(cudaMemcpy2DAsync(D.dB + w * K * ldb + s.b0 * ldb, ldb * 8,
                              B->base + w * pb_h + s.b0 * B->stride, B->stride * 8, n * 8,
-                             s.b1 - s.b0, cudaMemcpyHostToDevice, D.stream),
+                             s.b1 - s.b0, cudaMemcpyHostToDevice, D.up),
            "H2D B");
+    ck(cudaEventRecord(D.ev[1], D.up), "event");
+    const auto [nc, crows] = chunks_of(rows);
+    nchunks[g] = rows ? (int)nc : 0;
+    for (int c = 0; c < nchunks[g]; ++c) {
+      const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
+      for (int w = 0; w < W; ++w)
+        if (K)
+          ck(cudaMemcpy2DAsync(D.dA + w * rows * lda + c0 * lda, lda * 8,
+                               A->base + w * pa_h + (s.r0 + c0) * A->stride, A->stride * 8, K * 8,
+                               c1 - c0, cudaMemcpyHostToDevice, D.up),
+             "H2D A");
+      ck(cudaEventRecord(D.evA[c], D.up), "event");
     }
-    ck(cudaEventRecord(D.ev[1], D.stream), "event");
   };
-  auto phase2 = [&](int g) {  // gather the other B slices from peers, compute, download
+  auto phase2 = [&](int g) {  // gather B slices from peers, compute chunks, download chunks
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const uint64_t rows = s.r1 - s.r0;
+    ck(cudaStreamWaitEvent(D.stream, D.ev[1], 0), "wait B upload");
     if (peer) {
       for (int o = 0; o < G; ++o) {
         if (o == g || sh[o].b1 == sh[o].b0) continue;
@@ -428,22 +495,29 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
       }
     }
     ck(cudaEventRecord(D.ev[2], D.stream), "event");
-    launches[g] = rows ? enqueue_gemm(W, rows, n, K, D.dA, lda, rows * lda, D.dB, ldb, K * ldb,
-                                      D.dC, ldc, rows * ldc, D.stream)
-                       : 0;
-    ck(cudaEventRecord(D.ev[3], D.stream), "event");
-    for (int w = 0; w < W; ++w)
-      if (rows)
-        ck(cudaMemcpy2DAsync(C->base + w * pc_h + s.r0 * C->stride, C->stride * 8,
-                             D.dC + w * rows * ldc, ldc * 8, n * 8, rows, cudaMemcpyDeviceToHost,
-                             D.stream),
+    const uint64_t crows = nchunks[g] ? chunks_of(rows).second : 0;
+    for (int c = 0; c < nchunks[g]; ++c) {
+      const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
+      ck(cudaStreamWaitEvent(D.stream, D.evA[c], 0), "wait A chunk");
+      launches[g] += enqueue_gemm(W, c1 - c0, n, K, D.dA + c0 * lda, lda, rows * lda, D.dB, ldb,
+                                  K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, D.stream);
+      ck(cudaEventRecord(D.evC[c], D.stream), "event");
+      ck(cudaStreamWaitEvent(D.down, D.evC[c], 0), "wait C chunk");
+      for (int w = 0; w < W; ++w)
+        ck(cudaMemcpy2DAsync(C->base + w * pc_h + (s.r0 + c0) * C->stride, C->stride * 8,
+                             D.dC + w * rows * ldc + c0 * ldc, ldc * 8, n * 8, c1 - c0,
+                             cudaMemcpyDeviceToHost, D.down),
            "D2H C");
-    ck(cudaEventRecord(D.ev[4], D.stream), "event");
+    }
+    ck(cudaEventRecord(D.ev[3], D.stream), "event");
+    ck(cudaStreamWaitEvent(D.down, D.ev[3], 0), "join");
+    ck(cudaEventRecord(D.ev[4], D.down), "event");
     ck(cudaEventSynchronize(D.ev[4]), "GEMM execution");
-    cudaEventElapsedTime(&h2d[g], D.ev[0], D.ev[1]);
+    const cudaEvent_t h2d_end = nchunks[g] ? D.evA[nchunks[g] - 1] : D.ev[1];
+    cudaEventElapsedTime(&h2d[g], D.ev[0], h2d_end);
     cudaEventElapsedTime(&bc[g], D.ev[1], D.ev[2]);
     cudaEventElapsedTime(&kms[g], D.ev[2], D.ev[3]);
-    cudaEventElapsedTime(&d2h[g], D.ev[3], D.ev[4]);
+    cudaEventElapsedTime(&d2h[g], D.ev[3], D.ev[4]);  // exposed (non-overlapped) download tail
   };
   auto run_all = [&](auto&& fn) {
     if (G == 1) {
@@ -627,7 +701,11 @@ void mpfk_shutdown(void) {
     if (D.dB) cudaFree(D.dB);
     if (D.dC) cudaFree(D.dC);
     for (auto& e : D.ev) cudaEventDestroy(e);
+    for (auto& e : D.evA) cudaEventDestroy(e);
+    for (auto& e : D.evC) cudaEventDestroy(e);
     cudaStreamDestroy(D.stream);
+    cudaStreamDestroy(D.up);
+    cudaStreamDestroy(D.down);
     D = Device{};
   }
   g_dev.clear();
@@ -707,6 +785,94 @@ int mpfk_gemm_device(int width, uint64_t m, uint64_t n, uint64_t k, const double
     const int l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane,
                                static_cast<cudaStream_t>(stream));
     count_matmul(m, n, k);
+    if (launches) *launches = l;
+  });
+}
+
+int mpfk_ew_apply_into(int width, int op, mpfk_mat* out, const mpfk_mat* a, const mpfk_mat* b,
+                       int variant) {
+  return guarded([&] {
+    check_width(width);
+    check_mat(a, "a");
+    check_mat(b, "b");
+    check_mat(out, "out");
+    if (op < kern::EW_ADD || op > kern::EW_ADD_MERGE) fail(MPFK_EINVAL, "ew: unknown operation");
+    if (variant < MPFK_NORMAL || variant > MPFK_SIMD_LOADSTORE)
+      fail(MPFK_EINVAL, "ew: unknown kernel variant");
+    // linalg.hpp:650-653
+    if (!(a->rows == b->rows && a->cols == b->cols) || !(a->rows == out->rows && a->cols == out->cols))
+      fail(MPFK_EINVAL, "ew: shape mismatch");
+    if (op == kern::EW_ADD_MERGE && width != 3)
+      fail(MPFK_EINVAL, "ew: add_merge is a triple-width operation");
+    const uint64_t rows = a->rows, cols = a->cols;
+    mpfk_stats st{};
+    const auto t0 = std::chrono::steady_clock::now();
+    if (rows && cols) {
+      int dev = 0;
+      ck(cudaGetDevice(&dev), "cudaGetDevice");
+      ensure_devices(dev + 1);
+      Device& D = g_dev[dev];
+      const uint64_t ld = pad4(cols), ps = rows * ld;
+      grow(D.dA, D.capA, sizeof(double) * width * ps);
+      grow(D.dB, D.capB, sizeof(double) * width * ps);
+      grow(D.dC, D.capC, sizeof(double) * width * ps);
+      const uint64_t pa = plane_of(a), pb = plane_of(b), po = plane_of(out);
+      ck(cudaEventRecord(D.ev[0], D.stream), "event");
+      for (int w = 0; w < width; ++w) {
+        ck(cudaMemcpy2DAsync(D.dA + w * ps, ld * 8, a->base + w * pa, a->stride * 8, cols * 8, rows,
+                             cudaMemcpyHostToDevice, D.stream), "H2D a");
+        ck(cudaMemcpy2DAsync(D.dB + w * ps, ld * 8, b->base + w * pb, b->stride * 8, cols * 8, rows,
+                             cudaMemcpyHostToDevice, D.stream), "H2D b");
+      }
+      ck(cudaEventRecord(D.ev[1], D.stream), "event");
+      st.kernel_launches = enqueue_ew(width, op, rows, cols, D.dC, ld, ps, D.dA, ld, ps, D.dB, ld, ps,
+                                      D.stream);
+      ck(cudaEventRecord(D.ev[2], D.stream), "event");
+      for (int w = 0; w < width; ++w)
+        ck(cudaMemcpy2DAsync(out->base + w * po, out->stride * 8, D.dC + w * ps, ld * 8, cols * 8, rows,
+                             cudaMemcpyDeviceToHost, D.stream), "D2H out");
+      ck(cudaEventRecord(D.ev[3], D.stream), "event");
+      ck(cudaEventSynchronize(D.ev[3]), "ew execution");
+      float x = 0;
+      cudaEventElapsedTime(&x, D.ev[0], D.ev[1]);
+      st.h2d_ms = x;
+      cudaEventElapsedTime(&x, D.ev[1], D.ev[2]);
+      st.kernel_ms = x;
+      cudaEventElapsedTime(&x, D.ev[2], D.ev[3]);
+      st.d2h_ms = x;
+      st.h2d_bytes = 16ull * width * rows * cols;
+      st.d2h_bytes = 8ull * width * rows * cols;
+      st.n_gpus = 1;
+    }
+    // the SIMD variants run over the padding and restore it to +0
+    // (linalg.hpp:663-680); NORMAL leaves out's pads untouched (:654-657)
+    if (variant != MPFK_NORMAL) zero_host_pads(width, out);
+    count_ew(op, rows, cols);
+    st.total_ms = ms_since(t0);
+    t_stats = st;
+  });
+}
+
+int mpfk_ew_device(int width, int op, uint64_t rows, uint64_t cols, double* out, uint64_t ldo,
+                   uint64_t o_plane, const double* a, uint64_t lda, uint64_t a_plane, const double* b,
+                   uint64_t ldb, uint64_t b_plane, void* stream, int* launches) {
+  return guarded([&] {
+    check_width(width);
+    if (op < kern::EW_ADD || op > kern::EW_ADD_MERGE) fail(MPFK_EINVAL, "ew: unknown operation");
+    if (op == kern::EW_ADD_MERGE && width != 3)
+      fail(MPFK_EINVAL, "ew: add_merge is a triple-width operation");
+    if (ldo < cols || lda < cols || ldb < cols) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
+    if ((ldo | lda | ldb | o_plane | a_plane | b_plane) & 1)
+      fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
+         reinterpret_cast<uintptr_t>(b)) & 15)
+      fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ensure_devices(dev + 1);
+    const int l = enqueue_ew(width, op, rows, cols, out, ldo, o_plane, a, lda, a_plane, b, ldb, b_plane,
+                             static_cast<cudaStream_t>(stream));
+    count_ew(op, rows, cols);
     if (launches) *launches = l;
   });
 }

@@ -323,6 +323,74 @@ MPFK_HD void td_mul(const double* x, const double* y, double* r) {
   vseb_2_3(e1, e2, e3, r[1], r[2]);
 }
 
+// merge_by_magnitude, eft.hpp:229-236: stable merge of two 3-term lists by
+// nonincreasing magnitude (ties take x first), as the reference's loop
+// executes it for ANY input order: take x[i] while i < 3 and (j == 3 or
+// |x[i]| >= |y[j]|).
+MPFK_HD void merge6(const double* x, const double* y, double* z) {
+  int i = 0, j = 0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double xi = i == 0 ? x[0] : (i == 1 ? x[1] : x[2]);
+    const double yj = j == 0 ? y[0] : (j == 1 ? y[1] : y[2]);
+    const bool take_x = i < 3 && (j >= 3 || std::fabs(xi) >= std::fabs(yj));
+    z[k] = take_x ? xi : yj;
+    i += take_x ? 1 : 0;
+    j += take_x ? 0 : 1;
+  }
+}
+
+// VecSumErrBranch with k = 3 slots over n = 6 inputs (eft.hpp:205-225),
+// including its early exit once the last slot is final.
+MPFK_HD void vseb_3_6(const double* e, double* out) {
+  double o0 = 0.0, o1 = 0.0, o2 = 0.0;
+  int j = 0;
+  bool done = false;
+  double eps = e[0];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    double s, r;
+    qts(eps, e[i + 1], s, r);
+    if (!done) {
+      if (j == 0) o0 = s;
+      else if (j == 1) o1 = s;
+      else o2 = s;
+      if (nz(r)) {
+        if (j >= 2) {
+          done = true;
+        } else {
+          ++j;
+          eps = r;
+        }
+      } else {
+        eps = s;
+      }
+    }
+  }
+  if (!done && nz(eps)) {
+    if (j == 0) o0 = eps;
+    else if (j == 1) o1 = eps;
+    else o2 = eps;
+  }
+  out[0] = o0, out[1] = o1, out[2] = o2;
+}
+
+// td_add_merge, mpf.hpp:125-131: merge, distill (vec_sum<6>), compress.
+MPFK_HD void td_add_merge(const double* x, const double* y, double* r) {
+  double z[6], e[6];
+  merge6(x, y, z);
+  double s = z[5];
+#pragma unroll
+  for (int i = 4; i >= 0; --i) {
+    double ss, ee;
+    two_sum(z[i], s, ss, ee);
+    e[i + 1] = ee;
+    s = ss;
+  }
+  e[0] = s;
+  vseb_3_6(e, r);
+}
+
 // Library width defaults, mpf.hpp:242-260.
 template <int W>
 MPFK_HD void mp_add(const double* x, const double* y, double* r) {

@@ -213,6 +213,50 @@ def matmul_naive(A: MPMatrix, B: MPMatrix, variant: KernelVariant = KernelVarian
     return C_
 
 
+class EwOp(enum.IntEnum):
+    """linalg.hpp:623"""
+    add = 0
+    mul = 1
+    add_merge = 2
+
+
+def ew_apply_into(out: MPMatrix, a: MPMatrix, b: MPMatrix, op: EwOp,
+                  variant: KernelVariant = KernelVariant.NORMAL):
+    """linalg::ew_apply_into (linalg.hpp:647-684) on the GPU."""
+    W = _check_same_width(out, a, b)
+    o, x, y = out._c(), a._c(), b._c()
+    N.check(N.lib().mpfk_ew_apply_into(W, int(op), C.byref(o), C.byref(x), C.byref(y), int(variant)))
+
+
+def ew_add(a: MPMatrix, b: MPMatrix, variant: KernelVariant = KernelVariant.NORMAL) -> MPMatrix:
+    """linalg.hpp:686-692"""
+    r = MPMatrix(a.W, a.rows(), a.cols())
+    ew_apply_into(r, a, b, EwOp.add, variant)
+    return r
+
+
+def ew_mul(a: MPMatrix, b: MPMatrix, variant: KernelVariant = KernelVariant.NORMAL) -> MPMatrix:
+    """linalg.hpp:694-700"""
+    r = MPMatrix(a.W, a.rows(), a.cols())
+    ew_apply_into(r, a, b, EwOp.mul, variant)
+    return r
+
+
+def ew_add_merge(a: MPMatrix, b: MPMatrix, variant: KernelVariant = KernelVariant.NORMAL) -> MPMatrix:
+    """linalg.hpp:702-707 (triple width only)"""
+    r = MPMatrix(a.W, a.rows(), a.cols())
+    ew_apply_into(r, a, b, EwOp.add_merge, variant)
+    return r
+
+
+def ew_device(W: int, op: int, rows: int, cols: int, out_ptr: int, ldo: int, o_plane: int, a_ptr: int, lda: int,
+              a_plane: int, b_ptr: int, ldb: int, b_plane: int, stream: int = 0) -> int:
+    launches = C.c_int(0)
+    N.check(N.lib().mpfk_ew_device(W, int(op), rows, cols, out_ptr, ldo, o_plane, a_ptr, lda, a_plane, b_ptr, ldb,
+                                   b_plane, stream or None, C.byref(launches)))
+    return launches.value
+
+
 def op_counters_reset():
     N.lib().mpfk_op_counters_reset()
 

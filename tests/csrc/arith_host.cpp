@@ -36,6 +36,10 @@ void hst_td_add_unfolded_batch(std::size_t count, const double* x, const double*
   for (std::size_t i = 0; i < count; ++i) td_add_q_unfolded(x + 3 * i, y + 3 * i, r + 3 * i);
 }
 
+void hst_td_add_merge_batch(std::size_t count, const double* x, const double* y, double* r) {
+  for (std::size_t i = 0; i < count; ++i) td_add_merge(x + 3 * i, y + 3 * i, r + 3 * i);
+}
+
 void hst_renorm5_batch(std::size_t count, const double* c, double* r) {
   for (std::size_t i = 0; i < count; ++i) {
     const double* x = c + 5 * i;

@@ -149,3 +149,19 @@ def test_gemm_order_on_host(H, W):
         Cm = O.planes(W, m, n)
         H.hst_gemm(W, m, k, n, A.ctypes.data, A.shape[2], B.ctypes.data, B.shape[2], Cm.ctypes.data, Cm.shape[2])
         assert mismatches(Cm, O.ref_gemm(A, B, k, n)) == 0
+
+
+def test_td_add_merge_host(H):
+    """merge6 + vec_sum<6> + vseb(3 of 6) (mpf.hpp:125-131) vs the reference,
+    on sorted, unsorted and zero-laden inputs."""
+    H.hst_td_add_merge_batch.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
+    n = 40000
+    x = np.concatenate([_pairs(3, n // 2, 51), _special_values(3, n // 2, 52)])
+    y = np.concatenate([_pairs(3, n // 2, 53) * np.ldexp(1.0, np.random.default_rng(3).integers(-70, 70, (n // 2, 1))),
+                        _special_values(3, n // 2, 54)])
+    y[::5] = -x[::5]
+    r = np.empty_like(x)
+    H.hst_td_add_merge_batch(n, x.ctypes.data, y.ctypes.data, r.ctypes.data)
+    want = np.empty_like(x)
+    O.ref().ref_td_add_merge_batch(n, x.ctypes.data, y.ctypes.data, want.ctypes.data)
+    assert not (r.view(np.uint64) != want.view(np.uint64)).any()
