@@ -122,6 +122,18 @@ int mpfk_gemm_device(int width, uint64_t m, uint64_t n, uint64_t k, const double
                      uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, void *stream,
                      int *launches);
 
+/* Continuation over a K panel: C = C (+) A*B, i.e. every element's chain
+ * continues with add(C, mul(A(i,k), B(k,j))) for k = 0..k-1 of this panel.
+ * The reference carries the chain state in C between k steps
+ * (QuadRow::axpy reloads C, linalg.hpp:261), so a GEMM split into K panels
+ * -- the first through mpfk_gemm_device, the rest through this call, in
+ * ascending k -- is bit-identical to the one-shot product.  Lets a caller
+ * stream B (or A) in K panels and overlap the transfer with compute. */
+int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                         uint64_t lda, uint64_t a_plane, const double *B, uint64_t ldb,
+                         uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, void *stream,
+                         int *launches);
+
 /* ---- elementwise width kernels (mpf::add/mul<W>, mpf.hpp:341-353) ------- */
 
 /* EwOp, linalg.hpp:623 */
@@ -148,6 +160,28 @@ int mpfk_ew_device(int width, int op, uint64_t rows, uint64_t cols, double *out,
  * sweeps. */
 int mpfk_binop_batch(int width, int op, uint64_t count, const double *x, const double *y,
                      double *r);
+
+/* ---- MPFM matrix files (linalg_io.cpp:20-111, README.md:145-151) --------- */
+/* 33-byte header {"MPFM", u32 version 1, u8 width, u64 rows, cols, stride =
+ * pad4(cols)} + W little-endian binary64 planes, padding included and +0.
+ * Errors (MPFK_ERUNTIME) carry the reference's texts: "<path>: cannot open",
+ * "truncated", "not an MPFM file", "unsupported version", "component width
+ * mismatch", "implausible dimensions", "bad stride", "trailing data",
+ * "nonzero padding", "cannot open for writing", "write failed". */
+int mpfk_mpfm_info(const char *path, int *width, uint64_t *rows, uint64_t *cols);
+/* Stream a file's planes into device memory of the current device (any even
+ * or odd ld >= cols; plane stride >= rows*ld) through pinned double-buffered
+ * staging; returns once the data is on the device. */
+int mpfk_mpfm_load_device(const char *path, int width, double *dev, uint64_t ld, uint64_t plane,
+                          void *stream);
+/* Write rows x cols device cells as an MPFM file (pads written +0). */
+int mpfk_mpfm_save_device(const char *path, int width, const double *dev, uint64_t rows,
+                          uint64_t cols, uint64_t ld, uint64_t plane, void *stream);
+/* Host MPMatrix-layout forms: save_matrix_binary / load_matrix_binary
+ * (linalg_io.cpp:66-111); load requires m preallocated with the file's
+ * rows x cols (see mpfk_mpfm_info). */
+int mpfk_mpfm_load_host(const char *path, int width, mpfk_mat *m);
+int mpfk_mpfm_save_host(const char *path, int width, const mpfk_mat *m);
 
 /* ---- op counters (linalg.hpp:160-180, linalg.cpp:10-25) ----------------- */
 void mpfk_op_counters_reset(void);

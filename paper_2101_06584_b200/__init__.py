@@ -18,7 +18,13 @@ from .linalg import (  # noqa: F401
     format_eps,
     fp64_peak,
     gemm_device,
+    gemm_device_acc,
     last_stats,
+    load_matrix_binary,
+    mpfm_info,
+    mpfm_load_device,
+    mpfm_save_device,
+    save_matrix_binary,
     matmul_block,
     matmul_block_into,
     matmul_block_parallel,

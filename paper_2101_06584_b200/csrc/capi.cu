@@ -104,7 +104,10 @@ struct Device {
   cudaStream_t stream = nullptr;  // compute
   cudaStream_t up = nullptr;      // host->device copies
   cudaStream_t down = nullptr;    // device->host copies
+  cudaStream_t stream2 = nullptr; // second compute stream: chunk c+1 fills chunk c's tail
   cudaEvent_t ev[6] = {};
+  cudaEvent_t evB[kMaxChunks] = {};  // B K-panel p resident (single-GPU path)
+  cudaEvent_t evJ = nullptr;         // join of the second compute stream
   cudaEvent_t evA[kMaxChunks] = {};  // A row chunk c resident
   cudaEvent_t evC[kMaxChunks] = {};  // C row chunk c computed
   // grow-only operand buffers for the host-buffer path
@@ -178,6 +181,9 @@ void ensure_devices(int n) {
     ck(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&D.up, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&D.down, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&D.stream2, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : D.evB) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&D.evJ, cudaEventDisableTiming), "cudaEventCreate");
     for (auto& e : D.ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     for (auto& e : D.evA) ck(cudaEventCreate(&e), "cudaEventCreate");
     for (auto& e : D.evC) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
@@ -258,10 +264,13 @@ __global__ void zero_planes_kernel(double* C, long long ldc, long long pc, int M
 }
 
 // Enqueue C = A*B on the current device.  Returns kernel launches.
+// accumulate: continue the chains already in C over this K panel (see
+// GemmArgs::accumulate); k == 0 is then a no-op.
 int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
                  uint64_t pa, const double* B, uint64_t ldb, uint64_t pb, double* C,
-                 uint64_t ldc, uint64_t pc, cudaStream_t s) {
+                 uint64_t ldc, uint64_t pc, cudaStream_t s, bool accumulate = false) {
   if (m == 0 || n == 0) return 0;
+  if (k == 0 && accumulate) return 0;
   if (m > 0x7fffffffULL || n > 0x7fffffffULL || k > 0x7fffffffULL)
     fail(MPFK_EINVAL, "mpfk: dimension exceeds 2^31-1");
   if (k == 0) {
@@ -275,6 +284,7 @@ int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uin
   g.lda = (long long)lda, g.ldb = (long long)ldb, g.ldc = (long long)ldc;
   g.pa = (long long)pa, g.pb = (long long)pb, g.pc = (long long)pc;
   g.M = (int)m, g.N = (int)n, g.K = (int)k;
+  g.accumulate = accumulate ? 1 : 0;
   switch (W) {
     case 2:
       if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
@@ -446,8 +456,17 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     const uint64_t crows = ((rows + nc - 1) / nc + 63) / 64 * 64;
     return std::make_pair((rows + crows - 1) / std::max<uint64_t>(crows, 1), crows);
   };
+  // Single GPU: B is uploaded in K panels right after the first A chunk, and
+  // the first chunk's GEMM runs panel by panel (continuing the chains from C,
+  // bit-identical) so compute starts before all of B has landed.
+  auto panels_of = [&](uint64_t k) -> std::pair<int, uint64_t> {
+    if (peer || k < 1024) return {1, k};
+    const int np = (int)std::min<uint64_t>(kMaxChunks, k / 512);
+    const uint64_t pk = ((k + np - 1) / np + 15) / 16 * 16;  // even: 16-byte cp.async rows
+    return {(int)((k + pk - 1) / pk), pk};
+  };
   std::vector<int> nchunks(G, 0);
-  auto phase1 = [&](int g) {  // allocate; upload the B slice, then A row chunks
+  auto phase1 = [&](int g) {  // allocate; upload A chunk 0, B (slice or K panels), other A chunks
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -455,17 +474,10 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(rows * lda, 1));
     grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
     grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(rows * ldc, 1));
-    ck(cudaEventRecord(D.ev[0], D.up), "event");
-    for (int w = 0; w < W; ++w)
-      if (s.b1 > s.b0 && n)
-        ck(cudaMemcpy2DAsync(D.dB + w * K * ldb + s.b0 * ldb, ldb * 8,
-                             B->base + w * pb_h + s.b0 * B->stride, B->stride * 8, n * 8,
-                             s.b1 - s.b0, cudaMemcpyHostToDevice, D.up),
-           "H2D B");
-    ck(cudaEventRecord(D.ev[1], D.up), "event");
-    const auto [nc, crows] = chunks_of(rows);
+    const auto cpair = chunks_of(rows);
+    const uint64_t nc = cpair.first, crows = cpair.second;
     nchunks[g] = rows ? (int)nc : 0;
-    for (int c = 0; c < nchunks[g]; ++c) {
+    auto upload_a = [&](int c) {
       const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
       for (int w = 0; w < W; ++w)
         if (K)
@@ -474,15 +486,32 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
                                c1 - c0, cudaMemcpyHostToDevice, D.up),
              "H2D A");
       ck(cudaEventRecord(D.evA[c], D.up), "event");
+    };
+    ck(cudaEventRecord(D.ev[0], D.up), "event");
+    if (nchunks[g]) upload_a(0);
+    const auto ppair = panels_of(s.b1 - s.b0);
+    const int np = ppair.first;
+    const uint64_t pk = ppair.second;
+    for (int p = 0; p < np; ++p) {
+      const uint64_t k0 = s.b0 + p * pk, k1 = std::min<uint64_t>(s.b1, k0 + pk);
+      for (int w = 0; w < W; ++w)
+        if (k1 > k0 && n)
+          ck(cudaMemcpy2DAsync(D.dB + w * K * ldb + k0 * ldb, ldb * 8, B->base + w * pb_h + k0 * B->stride,
+                               B->stride * 8, n * 8, k1 - k0, cudaMemcpyHostToDevice, D.up),
+             "H2D B");
+      ck(cudaEventRecord(D.evB[p], D.up), "event");
     }
+    ck(cudaEventRecord(D.ev[1], D.up), "event");
+    for (int c = 1; c < nchunks[g]; ++c) upload_a(c);
   };
   auto phase2 = [&](int g) {  // gather B slices from peers, compute chunks, download chunks
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const uint64_t rows = s.r1 - s.r0;
-    ck(cudaStreamWaitEvent(D.stream, D.ev[1], 0), "wait B upload");
+    ck(cudaEventRecord(D.ev[2], D.stream), "event");
     if (peer) {
+      ck(cudaStreamWaitEvent(D.stream, D.ev[1], 0), "wait B upload");
       for (int o = 0; o < G; ++o) {
         if (o == g || sh[o].b1 == sh[o].b0) continue;
         Device& P = g_dev[sh[o].dev];
@@ -493,15 +522,31 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
                                  (sh[o].b1 - sh[o].b0) * ldb * 8, D.stream),
              "peer copy B");
       }
+      ck(cudaEventRecord(D.ev[5], D.stream), "event");  // B complete on this GPU
     }
-    ck(cudaEventRecord(D.ev[2], D.stream), "event");
+    const cudaEvent_t b_ready = peer ? D.ev[5] : D.ev[1];
     const uint64_t crows = nchunks[g] ? chunks_of(rows).second : 0;
+    const auto ppair = panels_of(K);
+    const int np = ppair.first;
+    const uint64_t pk = ppair.second;
     for (int c = 0; c < nchunks[g]; ++c) {
+      cudaStream_t cs = (c & 1) ? D.stream2 : D.stream;
       const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
-      ck(cudaStreamWaitEvent(D.stream, D.evA[c], 0), "wait A chunk");
-      launches[g] += enqueue_gemm(W, c1 - c0, n, K, D.dA + c0 * lda, lda, rows * lda, D.dB, ldb,
-                                  K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, D.stream);
-      ck(cudaEventRecord(D.evC[c], D.stream), "event");
+      ck(cudaStreamWaitEvent(cs, D.evA[c], 0), "wait A chunk");
+      if (c == 0 && np > 1) {
+        for (int p = 0; p < np; ++p) {
+          const uint64_t k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
+          ck(cudaStreamWaitEvent(cs, D.evB[p], 0), "wait B panel");
+          launches[g] += enqueue_gemm(W, c1 - c0, n, k1 - k0, D.dA + c0 * lda + k0, lda, rows * lda,
+                                      D.dB + k0 * ldb, ldb, K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs,
+                                      p > 0);
+        }
+      } else {
+        ck(cudaStreamWaitEvent(cs, b_ready, 0), "wait B");
+        launches[g] += enqueue_gemm(W, c1 - c0, n, K, D.dA + c0 * lda, lda, rows * lda, D.dB, ldb,
+                                    K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs);
+      }
+      ck(cudaEventRecord(D.evC[c], cs), "event");
       ck(cudaStreamWaitEvent(D.down, D.evC[c], 0), "wait C chunk");
       for (int w = 0; w < W; ++w)
         ck(cudaMemcpy2DAsync(C->base + w * pc_h + (s.r0 + c0) * C->stride, C->stride * 8,
@@ -509,15 +554,17 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
                              cudaMemcpyDeviceToHost, D.down),
            "D2H C");
     }
+    ck(cudaEventRecord(D.evJ, D.stream2), "event");
+    ck(cudaStreamWaitEvent(D.stream, D.evJ, 0), "join");
     ck(cudaEventRecord(D.ev[3], D.stream), "event");
     ck(cudaStreamWaitEvent(D.down, D.ev[3], 0), "join");
     ck(cudaEventRecord(D.ev[4], D.down), "event");
     ck(cudaEventSynchronize(D.ev[4]), "GEMM execution");
-    const cudaEvent_t h2d_end = nchunks[g] ? D.evA[nchunks[g] - 1] : D.ev[1];
+    const cudaEvent_t h2d_end = nchunks[g] > 1 ? D.evA[nchunks[g] - 1] : D.ev[1];
     cudaEventElapsedTime(&h2d[g], D.ev[0], h2d_end);
-    cudaEventElapsedTime(&bc[g], D.ev[1], D.ev[2]);
-    cudaEventElapsedTime(&kms[g], D.ev[2], D.ev[3]);
-    cudaEventElapsedTime(&d2h[g], D.ev[3], D.ev[4]);  // exposed (non-overlapped) download tail
+    bc[g] = 0.f;
+    cudaEventElapsedTime(&kms[g], D.ev[2], D.ev[3]);  // compute span incl. waits for data
+    cudaEventElapsedTime(&d2h[g], D.ev[3], D.ev[4]);  // exposed download tail
   };
   auto run_all = [&](auto&& fn) {
     if (G == 1) {
@@ -664,6 +711,8 @@ void baseline_elem(int W, int wide, SM64& g, double* v) {
     renormalize_host(W, c, v);
 }
 
+#include "mpfm_io.inl"
+
 }  // namespace
 
 // ===========================================================================
@@ -706,6 +755,9 @@ void mpfk_shutdown(void) {
     cudaStreamDestroy(D.stream);
     cudaStreamDestroy(D.up);
     cudaStreamDestroy(D.down);
+    cudaStreamDestroy(D.stream2);
+    for (auto& e : D.evB) cudaEventDestroy(e);
+    cudaEventDestroy(D.evJ);
     D = Device{};
   }
   g_dev.clear();
@@ -877,6 +929,30 @@ int mpfk_ew_device(int width, int op, uint64_t rows, uint64_t cols, double* out,
   });
 }
 
+int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                         uint64_t a_plane, const double* B, uint64_t ldb, uint64_t b_plane, double* C,
+                         uint64_t ldc, uint64_t c_plane, void* stream, int* launches) {
+  return guarded([&] {
+    check_width(width);
+    if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
+    if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
+      fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+         reinterpret_cast<uintptr_t>(C)) & 15)
+      fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ensure_devices(dev + 1);
+    const int l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane,
+                               static_cast<cudaStream_t>(stream), true);
+    if (k) {  // k more multiply-adds per element: k muls and k adds
+      g_muls.fetch_add(m * n * k, std::memory_order_relaxed);
+      g_adds.fetch_add(m * n * k, std::memory_order_relaxed);
+    }
+    if (launches) *launches = l;
+  });
+}
+
 int mpfk_binop_batch(int width, int op, uint64_t count, const double* x, const double* y,
                      double* r) {
   return guarded([&] {
@@ -904,6 +980,66 @@ int mpfk_binop_batch(int width, int op, uint64_t count, const double* x, const d
     cudaFree(dx);
     cudaFree(dy);
     cudaFree(dr);
+  });
+}
+
+int mpfk_mpfm_info(const char* path, int* width, uint64_t* rows, uint64_t* cols) {
+  return guarded([&] {
+    const std::string p = path ? path : "";
+    File F;
+    F.f = std::fopen(p.c_str(), "rb");
+    if (!F.f) io_fail(p, "cannot open");
+    const MpfmHeader h = read_header(F.f, p, 0);
+    if (width) *width = h.width;
+    if (rows) *rows = h.rows;
+    if (cols) *cols = h.cols;
+  });
+}
+
+int mpfk_mpfm_load_device(const char* path, int width, double* dev, uint64_t ld, uint64_t plane,
+                          void* stream) {
+  return guarded([&] {
+    check_width(width);
+    int d = 0;
+    ck(cudaGetDevice(&d), "cudaGetDevice");
+    ensure_devices(d + 1);
+    mpfm_load(path, width, dev, ld, plane, true, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mpfk_mpfm_save_device(const char* path, int width, const double* dev, uint64_t rows, uint64_t cols,
+                          uint64_t ld, uint64_t plane, void* stream) {
+  return guarded([&] {
+    check_width(width);
+    int d = 0;
+    ck(cudaGetDevice(&d), "cudaGetDevice");
+    ensure_devices(d + 1);
+    mpfm_save(path, width, dev, rows, cols, ld, plane, true, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mpfk_mpfm_load_host(const char* path, int width, mpfk_mat* m) {
+  return guarded([&] {
+    check_width(width);
+    check_mat(m, "m");
+    const std::string p = path ? path : "";
+    {
+      File F;
+      F.f = std::fopen(p.c_str(), "rb");
+      if (!F.f) io_fail(p, "cannot open");
+      const MpfmHeader h = read_header(F.f, p, width);
+      if (h.rows != m->rows || h.cols != m->cols) fail(MPFK_EINVAL, "mpfk: matrix shape differs from the file");
+    }
+    zero_host_pads(width, m);
+    mpfm_load(path, width, m->base, m->stride, plane_of(m), false, nullptr);
+  });
+}
+
+int mpfk_mpfm_save_host(const char* path, int width, const mpfk_mat* m) {
+  return guarded([&] {
+    check_width(width);
+    check_mat(m, "m");
+    mpfm_save(path, width, m->base, m->rows, m->cols, m->stride, plane_of(m), false, nullptr);
   });
 }
 

@@ -34,6 +34,12 @@ struct GemmArgs {
   long long lda, ldb, ldc;
   long long pa, pb, pc;
   int M, N, K;
+  // 0: C = A*B (k = 0 initialises, linalg.hpp:242).  1: continue the chains
+  // stored in C over this K panel: every k is an add(C, mul(a, b)).  The
+  // reference itself carries the chain state in C between k steps
+  // (QuadRow::axpy reloads C, linalg.hpp:261), so splitting K into panels
+  // and continuing from C is bit-identical.
+  int accumulate;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -128,6 +134,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   const int ktiles = (g.K + BK - 1) / BK;
 
   double acc[TM][TN][W];
+  if (g.accumulate) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int gm = m0 + ty + i * TY, gn = n0 + tx + j * TX;
+        const bool ok = gm < g.M && gn < g.N;
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[i][j][w] = ok ? g.C[w * g.pc + (long long)gm * g.ldc + gn] : 0.0;
+      }
+  }
 
   // prologue: fill STAGES-1 stages
 #pragma unroll
@@ -154,7 +171,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     const double* Bs = Bs0 + slot * Cfg::B_STAGE;
     const int kend = min(BK, g.K - kt * BK);
     int kk = 0;
-    if (kt == 0) {
+    if (kt == 0 && !g.accumulate) {
       // k == 0: the product initialises the element (linalg.hpp:242, 260-261)
       double a[TM][W], b[TN][W];
 #pragma unroll

@@ -86,6 +86,7 @@ int tune_run(int i, int M, int N, int K, const double* A, long long lda, long lo
   g.A = A, g.B = B, g.C = C;
   g.lda = lda, g.ldb = ldb, g.ldc = ldc, g.pa = pa, g.pb = pb, g.pc = pc;
   g.M = M, g.N = N, g.K = K;
+  g.accumulate = 0;
   return (int)kEntries[i].run(g, (cudaStream_t)stream);
 }
 }

@@ -257,6 +257,44 @@ def ew_device(W: int, op: int, rows: int, cols: int, out_ptr: int, ldo: int, o_p
     return launches.value
 
 
+# --- MPFM matrix files (linalg_io.cpp:66-111) ----------------------------------
+
+def mpfm_info(path: str):
+    """(width, rows, cols) from an MPFM header (validated)."""
+    w, r, c = C.c_int(), C.c_uint64(), C.c_uint64()
+    N.check(N.lib().mpfk_mpfm_info(path.encode(), C.byref(w), C.byref(r), C.byref(c)))
+    return w.value, r.value, c.value
+
+
+def save_matrix_binary(m: MPMatrix, path: str):
+    """linalg::save_matrix_binary (linalg_io.cpp:66-83)."""
+    x = m._c()
+    N.check(N.lib().mpfk_mpfm_save_host(path.encode(), m.W, C.byref(x)))
+
+
+def load_matrix_binary(W: int, path: str, pinned: bool = False) -> MPMatrix:
+    """linalg::load_matrix_binary<W> (linalg_io.cpp:85-111)."""
+    w, r, c = C.c_int(), C.c_uint64(), C.c_uint64()
+    N.check(N.lib().mpfk_mpfm_info(path.encode(), C.byref(w), C.byref(r), C.byref(c)))
+    if w.value != W:
+        raise RuntimeError(f"{path}: component width mismatch")
+    m = MPMatrix(W, r.value, c.value, pinned=pinned)
+    x = m._c()
+    N.check(N.lib().mpfk_mpfm_load_host(path.encode(), W, C.byref(x)))
+    return m
+
+
+def mpfm_load_device(path: str, W: int, dev_ptr: int, ld: int, plane: int, stream: int = 0):
+    """Stream an MPFM file into device memory (current device)."""
+    N.check(N.lib().mpfk_mpfm_load_device(path.encode(), W, dev_ptr, ld, plane, stream or None))
+
+
+def mpfm_save_device(path: str, W: int, dev_ptr: int, rows: int, cols: int, ld: int, plane: int,
+                     stream: int = 0):
+    """Write device-resident planes as an MPFM file."""
+    N.check(N.lib().mpfk_mpfm_save_device(path.encode(), W, dev_ptr, rows, cols, ld, plane, stream or None))
+
+
 def op_counters_reset():
     N.lib().mpfk_op_counters_reset()
 
@@ -282,6 +320,15 @@ def gemm_device(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: i
     launches = C.c_int(0)
     N.check(N.lib().mpfk_gemm_device(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
                                      c_plane, stream or None, C.byref(launches)))
+    return launches.value
+
+
+def gemm_device_acc(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int, ldb: int,
+                    b_plane: int, C_ptr: int, ldc: int, c_plane: int, stream: int = 0) -> int:
+    """Continue the chains in C over one K panel (mpfk_gemm_device_acc)."""
+    launches = C.c_int(0)
+    N.check(N.lib().mpfk_gemm_device_acc(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
+                                         c_plane, stream or None, C.byref(launches)))
     return launches.value
 
 

@@ -222,3 +222,26 @@ def test_device_api_with_torch_stream(gpu_lib):
     s.synchronize()
     assert launches == 1
     assert mismatches(dC.cpu().numpy(), O.ref_gemm(A, B, k, n)) == 0
+
+
+@pytest.mark.parametrize("W", WIDTHS)
+def test_k_panel_continuation_bitwise(gpu_lib, W):
+    """C from mpfk_gemm_device over panel 0 then mpfk_gemm_device_acc over
+    the remaining K panels (uneven, even-aligned splits) == one-shot C ==
+    reference: the chain state between k steps is exactly C (linalg.hpp:261)."""
+    import torch
+    P = gpu_lib
+    m, k, n = 45, 203, 37
+    A = random_signed(W, m, k, 880 + W)
+    B = random_signed(W, k, n, 890 + W)
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    lda, ldb = A.shape[2], B.shape[2]
+    dC = torch.zeros((W, m, ldb), dtype=torch.float64, device="cuda")
+    cuts = [0, 16, 18, 100, 150, k]
+    for p, (k0, k1) in enumerate(zip(cuts, cuts[1:])):
+        f = P.gemm_device if p == 0 else P.gemm_device_acc
+        f(W, m, n, k1 - k0, dA.data_ptr() + 8 * k0, lda, m * lda, dB.data_ptr() + 8 * k0 * ldb, ldb, k * ldb,
+          dC.data_ptr(), ldb, m * ldb)
+    torch.cuda.synchronize()
+    assert mismatches(dC.cpu().numpy(), O.ref_gemm(A, B, k, n)) == 0
