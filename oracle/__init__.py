@@ -40,6 +40,7 @@ def orc():
         L.orc_gemm.argtypes = [C.c_int, _S, _S, _S, _D, _S, _D, _S, _D, _S]
         L.orc_gemm_rows.argtypes = [C.c_int, _S, _S, _S, _D, _S, _D, _S, _D, _S, _S, _S]
         L.orc_add.argtypes = [C.c_int, _D, _D, _D]
+        L.orc_gemm_acc.argtypes = [C.c_int, _S, _S, _S, _D, _S, _S, _D, _S, _S, _D, _S, _S]
         L.orc_mul.argtypes = [C.c_int, _D, _D, _D]
         L.orc_renorm5.argtypes = [_D, _D]
         L.orc_vseb.argtypes = [_D, _S, _D, _S]

@@ -159,8 +159,11 @@ void run_selftest_current() {
          "the extended-precision kernels are unusable in this environment");
 }
 
-// Lazily initialise devices [0, n).  Caller holds no lock.
-void ensure_devices(int n) {
+// Lazily initialise `n` devices starting at `first` (wrapping), e.g. the
+// caller's current device and its successors.  Only those devices get a
+// context, so one process per GPU (torchrun) touches only its own GPU.
+// Caller holds no lock.
+void ensure_devices(int n, int first = 0) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (g_ndev < 0) {
     g_ndev = visible_sm100_devices();
@@ -173,7 +176,8 @@ void ensure_devices(int n) {
   if (n > g_ndev) n = g_ndev;
   int prev = 0;
   cudaGetDevice(&prev);
-  for (int d = 0; d < n; ++d) {
+  for (int i = 0; i < n; ++i) {
+    const int d = (first + i) % g_ndev;
     Device& D = g_dev[d];
     if (D.ready) continue;
     ck(cudaSetDevice(d), "cudaSetDevice");
@@ -190,6 +194,24 @@ void ensure_devices(int n) {
     D.ready = true;
   }
   cudaSetDevice(prev);
+}
+
+// The caller's current device; MPFK_ENODEV (no fallback) when none is usable.
+int current_device() {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_ndev < 0) {
+      g_ndev = visible_sm100_devices();
+      g_dev.resize(std::max(g_ndev, 0));
+      for (int d = 0; d < g_ndev; ++d) g_dev[d].id = d;
+    }
+    if (g_ndev == 0)
+      fail(MPFK_ENODEV,
+           "mpfk: no CUDA sm_100 device is visible; the GPU library has no CPU fallback");
+  }
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  return dev;
 }
 
 void grow(double*& p, size_t& cap, size_t bytes) {
@@ -404,7 +426,8 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     t_stats = st;
     return;
   }
-  ensure_devices((int)gpus);
+  const int base = current_device();
+  ensure_devices((int)gpus, base);
   int G = std::min<int>((int)gpus, g_ndev);
   // never more GPUs than 64-row blocks, like nt = min(workers, nblocks)
   G = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)G, (m + 63) / 64));
@@ -416,7 +439,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   const uint64_t per = ((m + G - 1) / G + 63) / 64 * 64;
   const uint64_t bper = (K + G - 1) / G;
   for (int g = 0; g < G; ++g) {
-    sh[g].dev = g;
+    sh[g].dev = (base + g) % g_ndev;  // the caller's device first
     sh[g].r0 = std::min<uint64_t>(m, g * per);
     sh[g].r1 = std::min<uint64_t>(m, (g + 1) * per);
     sh[g].b0 = G == 1 ? 0 : std::min<uint64_t>(K, g * bper);
@@ -426,13 +449,13 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   if (peer) {
     std::lock_guard<std::mutex> lk(g_mu);
     for (int a = 0; a < G; ++a) {
-      ck(cudaSetDevice(a), "cudaSetDevice");
+      ck(cudaSetDevice(sh[a].dev), "cudaSetDevice");
       for (int b = 0; b < G; ++b) {
         if (a == b) continue;
         int can = 0;
-        cudaDeviceCanAccessPeer(&can, a, b);
+        cudaDeviceCanAccessPeer(&can, sh[a].dev, sh[b].dev);
         if (!can) fail(MPFK_ECUDA, "mpfk: GPUs lack peer access for the B all-gather");
-        cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        cudaError_t e = cudaDeviceEnablePeerAccess(sh[b].dev, 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "enable peer");
         cudaGetLastError();
       }
@@ -831,9 +854,8 @@ int mpfk_gemm_device(int width, uint64_t m, uint64_t n, uint64_t k, const double
     if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
          reinterpret_cast<uintptr_t>(C)) & 15)
       fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
-    int dev = 0;
-    ck(cudaGetDevice(&dev), "cudaGetDevice");
-    ensure_devices(dev + 1);
+    const int dev = current_device();
+    ensure_devices(1, dev);
     const int l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane,
                                static_cast<cudaStream_t>(stream));
     count_matmul(m, n, k);
@@ -860,9 +882,8 @@ int mpfk_ew_apply_into(int width, int op, mpfk_mat* out, const mpfk_mat* a, cons
     mpfk_stats st{};
     const auto t0 = std::chrono::steady_clock::now();
     if (rows && cols) {
-      int dev = 0;
-      ck(cudaGetDevice(&dev), "cudaGetDevice");
-      ensure_devices(dev + 1);
+      const int dev = current_device();
+      ensure_devices(1, dev);
       Device& D = g_dev[dev];
       const uint64_t ld = pad4(cols), ps = rows * ld;
       grow(D.dA, D.capA, sizeof(double) * width * ps);
@@ -919,9 +940,8 @@ int mpfk_ew_device(int width, int op, uint64_t rows, uint64_t cols, double* out,
     if ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
          reinterpret_cast<uintptr_t>(b)) & 15)
       fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
-    int dev = 0;
-    ck(cudaGetDevice(&dev), "cudaGetDevice");
-    ensure_devices(dev + 1);
+    const int dev = current_device();
+    ensure_devices(1, dev);
     const int l = enqueue_ew(width, op, rows, cols, out, ldo, o_plane, a, lda, a_plane, b, ldb, b_plane,
                              static_cast<cudaStream_t>(stream));
     count_ew(op, rows, cols);
@@ -940,9 +960,8 @@ int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const do
     if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
          reinterpret_cast<uintptr_t>(C)) & 15)
       fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
-    int dev = 0;
-    ck(cudaGetDevice(&dev), "cudaGetDevice");
-    ensure_devices(dev + 1);
+    const int dev = current_device();
+    ensure_devices(1, dev);
     const int l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane,
                                static_cast<cudaStream_t>(stream), true);
     if (k) {  // k more multiply-adds per element: k muls and k adds
@@ -959,9 +978,8 @@ int mpfk_binop_batch(int width, int op, uint64_t count, const double* x, const d
     check_width(width);
     if (op != 0 && op != 1) fail(MPFK_EINVAL, "mpfk: op must be 0 (add) or 1 (mul)");
     if (count == 0) return;
-    int dev = 0;
-    ck(cudaGetDevice(&dev), "cudaGetDevice");
-    ensure_devices(dev + 1);
+    const int dev = current_device();
+    ensure_devices(1, dev);
     const size_t bytes = sizeof(double) * width * count;
     double *dx = nullptr, *dy = nullptr, *dr = nullptr;
     ck(cudaMalloc(&dx, bytes), "cudaMalloc");
@@ -1000,9 +1018,8 @@ int mpfk_mpfm_load_device(const char* path, int width, double* dev, uint64_t ld,
                           void* stream) {
   return guarded([&] {
     check_width(width);
-    int d = 0;
-    ck(cudaGetDevice(&d), "cudaGetDevice");
-    ensure_devices(d + 1);
+    const int d = current_device();
+    ensure_devices(1, d);
     mpfm_load(path, width, dev, ld, plane, true, static_cast<cudaStream_t>(stream));
   });
 }
@@ -1011,9 +1028,8 @@ int mpfk_mpfm_save_device(const char* path, int width, const double* dev, uint64
                           uint64_t ld, uint64_t plane, void* stream) {
   return guarded([&] {
     check_width(width);
-    int d = 0;
-    ck(cudaGetDevice(&d), "cudaGetDevice");
-    ensure_devices(d + 1);
+    const int d = current_device();
+    ensure_devices(1, d);
     mpfm_save(path, width, dev, rows, cols, ld, plane, true, static_cast<cudaStream_t>(stream));
   });
 }
@@ -1103,9 +1119,8 @@ int mpfk_fill_baseline(int width, int wide, uint64_t row0, uint64_t rows, uint64
 
 int mpfk_fp64_peak(double* ops_per_s, double* ms_out) {
   return guarded([&] {
-    int dev = 0;
-    ck(cudaGetDevice(&dev), "cudaGetDevice");
-    ensure_devices(dev + 1);
+    const int dev = current_device();
+    ensure_devices(1, dev);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     double* d = nullptr;

@@ -48,9 +48,58 @@ def sharded_gemm_step(W: int, dA, dB, dC, rows: int, n: int, k: int, ld: int, *,
     if gemm is None:
         from . import linalg as L
         s = stream.cuda_stream if stream is not None else 0
-        return L.gemm_device(W, rows, n, k, dA.data_ptr(), ld, rows * ld, dB.data_ptr(), ld, k * ld,
-                             dC.data_ptr(), ld, rows * ld, s)
+        lda, ldb, ldc = dA.shape[2], dB.shape[2], dC.shape[2]
+        return L.gemm_device(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
+                             dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, s)
     return gemm(W, dA, dB, dC, rows, n, k, ld)
+
+
+def k_panels(k: int, panels: int, align: int = 16):
+    """Split [0, k) into <= panels contiguous K panels whose starts are
+    multiples of `align` (even offsets keep 16-byte cp.async rows)."""
+    panels = max(1, min(panels, k // align if k >= align else 1))
+    pk = ((k + panels - 1) // panels + align - 1) // align * align
+    return [(k0, min(k, k0 + pk)) for k0 in range(0, k, pk)] or [(0, 0)]
+
+
+def sharded_gemm_step_overlapped(W: int, dA, dB, dC, rows: int, n: int, k: int, ld: int, *, panels: int = 4,
+                                 stream=None, gemm: Optional[Callable] = None, group=None) -> int:
+    """One sharded step with the B replication overlapped with compute: B is
+    broadcast in K panels (one asynchronous NCCL broadcast per panel and
+    component plane, all queued at once), and the rank's GEMM runs panel by
+    panel -- panel 0 with mpfk_gemm_device, later panels with
+    mpfk_gemm_device_acc continuing the chains stored in C -- each launch
+    gated only on its own panel's broadcast.  Bit-identical to
+    sharded_gemm_step (the chain state between k steps is exactly C,
+    linalg.hpp:261).
+
+    `gemm(W, A_panel, B_panel, dC, rows, n, kp, ld, accumulate)` overrides
+    the device kernel (the CPU tests pass the oracle)."""
+    import torch.distributed as dist
+    parts = k_panels(k, panels)
+    multi = dist.is_initialized() and dist.get_world_size(group) > 1
+    works = []
+    if multi:
+        for k0, k1 in parts:
+            works.append([dist.broadcast(dB[w, k0:k1], src=0, group=group, async_op=True) for w in range(W)])
+    launches = 0
+    for p, (k0, k1) in enumerate(parts):
+        if multi:
+            for wk in works[p]:
+                wk.wait()  # the compute stream waits for this panel only
+        if rows == 0 or k1 == k0:
+            continue
+        if gemm is not None:
+            launches += gemm(W, dA[:, :, k0:k1], dB[:, k0:k1], dC, rows, n, k1 - k0, ld, p > 0)
+            continue
+        from . import linalg as L
+        s = stream.cuda_stream if stream is not None else 0
+        f = L.gemm_device if p == 0 else L.gemm_device_acc
+        lda, ldb, ldc = dA.shape[2], dB.shape[2], dC.shape[2]
+        launches += f(W, rows, n, k1 - k0, dA.data_ptr() + 8 * k0, lda, dA.shape[1] * lda,
+                      dB.data_ptr() + 8 * k0 * ldb, ldb, dB.shape[1] * ldb, dC.data_ptr(), ldc,
+                      dC.shape[1] * ldc, s)
+    return launches
 
 
 def gather_c(dC_shard, m: int, world: int, group=None, align: int = 64):

@@ -81,3 +81,62 @@ def test_two_rank_gloo_row_shards_bit_identical(W, m, k, n):
     assert all(p.exitcode == 0 for p in procs)
     same, launches = q.get(timeout=10)
     assert same and launches == 1
+
+
+def _worker_overlapped(rank, world, port, W, m, k, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ctypes as C
+
+        import oracle as O
+        from paper_2101_06584_b200.dist import sharded_gemm_step_overlapped
+        ld = (n + 3) & ~3
+        A = O.orc_fill_baseline(W, m, k, 1, wide=True)
+        r0, r1 = shard_rows(m, world, rank, align=8)
+        rows = r1 - r0
+        dA = torch.from_numpy(np.ascontiguousarray(A[:, r0:r1]))
+        dB = torch.zeros((W, k, ld), dtype=torch.float64)
+        if rank == 0:
+            dB.copy_(torch.from_numpy(O.orc_fill_baseline(W, k, n, 2, wide=True)))
+        dC = torch.zeros((W, max(rows, 1), ld), dtype=torch.float64)
+
+        def oracle_panel(W_, Ap, Bp, dC_, rows_, n_, kp, ld_, acc):
+            a = np.ascontiguousarray(Ap.numpy())
+            b = np.ascontiguousarray(Bp.numpy())
+            if not acc:
+                dC_[:, :rows_] = torch.from_numpy(O.orc_gemm(a, b, kp, n_))
+            else:
+                c = np.ascontiguousarray(dC_[:, :rows_].numpy())
+                O.orc().orc_gemm_acc(W_, rows_, kp, n_, a.ctypes.data, a.shape[2], a.shape[1] * a.shape[2],
+                                     b.ctypes.data, b.shape[2], b.shape[1] * b.shape[2], c.ctypes.data,
+                                     c.shape[2], c.shape[1] * c.shape[2])
+                dC_[:, :rows_] = torch.from_numpy(c)
+            return 1
+
+        launches = sharded_gemm_step_overlapped(W, dA, dB, dC, rows, n, k, ld, panels=3, gemm=oracle_panel)
+        Cfull = gather_c(dC[:, :rows], m, world, align=8)
+        if rank == 0:
+            want = O.orc_gemm(A, O.orc_fill_baseline(W, k, n, 2, wide=True), k, n)
+            q.put((np.array_equal(Cfull.numpy().view(np.uint64), want.view(np.uint64)), launches))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("W,m,k,n", [(2, 21, 50, 13), (4, 12, 40, 7)])
+def test_two_rank_gloo_overlapped_k_panels(W, m, k, n):
+    """B broadcast in K panels overlapped with per-panel continuation GEMMs:
+    bit-identical to the one-shot product (linalg.hpp:261)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_overlapped, args=(r, 2, port, W, m, k, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    same, launches = q.get(timeout=10)
+    from paper_2101_06584_b200.dist import k_panels
+    assert same and launches == len(k_panels(k, 3)) > 1
