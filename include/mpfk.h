@@ -106,6 +106,16 @@ int mpfk_matmul_block_into(int width, mpfk_mat *C, const mpfk_mat *A, const mpfk
 /* matmul_naive_into, linalg.hpp:346-358 (same result by construction) */
 int mpfk_matmul_naive_into(int width, mpfk_mat *C, const mpfk_mat *A, const mpfk_mat *B,
                            int variant);
+/* matmul_strassen / matmul_strassen_parallel (linalg.hpp:582-617) into a
+ * caller-allocated m x n C: Strassen top levels on the GPU (per-level even
+ * zero padding, the fixed M1..M7 operand order, exact width add/sub) with
+ * the block GEMM as the leaf once min(m, K, n) <= cutoff.  Bit-identical to
+ * the reference's Strassen (not to the block product -- a different
+ * algorithm).  Errors as the reference ("matmul: cutoff must be at least
+ * 1", ...).  Counts adds per mat_add/mat_sub, leaf multiplies, and each
+ * leaf's count_matmul, like linalg.hpp:457, :468, :570. */
+int mpfk_matmul_strassen(int width, mpfk_mat *C, const mpfk_mat *A, const mpfk_mat *B,
+                         uint64_t cutoff, uint64_t n_min, int variant, unsigned workers);
 int mpfk_last_stats(mpfk_stats *out);
 
 /* ---- GEMM, device-resident operands ------------------------------------ */
@@ -203,6 +213,15 @@ void mpfk_host_free(void *p);
  * threads <= 0: hardware concurrency. */
 int mpfk_fill_baseline(int width, int wide, uint64_t row0, uint64_t rows, uint64_t cols,
                        uint64_t stride, uint64_t seed, double *planes, int threads);
+
+/* bench::fill_random (bench.cpp:295-302): one sequential SplitMix64 stream
+ * from `seed` over the matrix in row-major order, each element
+ * rng::random_normalized<W> (random.hpp:54-67, lead in [1,2)). */
+int mpfk_fill_random(int width, uint64_t rows, uint64_t cols, uint64_t stride, uint64_t seed,
+                     double *planes);
+/* bench::gen_paper_matrices (bench.cpp:278-292): A(i,j) = sqrt5 * (i+j-1),
+ * B(i,j) = sqrt3 * (n-i) (1-based), products taken in width W. */
+int mpfk_gen_paper(int width, uint64_t n, uint64_t stride, double *A, double *B);
 
 /* FP64 pipe microbenchmark on the current device: returns measured FP64
  * lane-operations per second (each DADD/DMUL/DFMA counted once), the

@@ -82,6 +82,8 @@ def ref():
         L.ref_op_counts.argtypes = [_D, _D]
         L.ref_random_normalized.argtypes = [C.c_int, _D, C.c_int, _D]
         L.ref_hardware_concurrency.restype = C.c_uint
+        L.ref_strassen.argtypes = [C.c_int, _S, _S, _S, _D, _S, _D, _S, _D, _S, _S, _S, C.c_int, C.c_uint]
+        L.ref_leaf_multiplies.restype = _U64
         L.ref_ew.argtypes = [C.c_int, C.c_int, C.c_int, _S, _S, _D, _S, _D, _S, _D, _S]
         L.ref_td_add_merge_batch.argtypes = [_S, _D, _D, _D]
         _ref = L
@@ -187,3 +189,17 @@ def ref_ew(W, op, a, b, cols, variant=0):
     if rc:
         raise ValueError(ref().ref_last_error().decode())
     return out
+
+
+def ref_strassen(A, B, K, n, cutoff=64, n_min=32, variant=0, workers=1):
+    """The reference's matmul_strassen / matmul_strassen_parallel."""
+    W, m, lda = A.shape
+    ldb = B.shape[2]
+    ldc = (n + 3) & ~3
+    Cm = np.zeros((W, m, ldc), dtype=np.float64)
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    rc = ref().ref_strassen(W, m, K, n, _p(A), lda, _p(B), ldb, _p(Cm), ldc, cutoff, n_min, variant, workers)
+    if rc:
+        raise ValueError(ref().ref_last_error().decode())
+    return Cm

@@ -208,6 +208,29 @@ int ref_binop(int W, int op, const double* x, const double* y, double* r) {
   return 0;
 }
 
+// linalg::matmul_strassen[_parallel] (linalg.hpp:582-617); leaf counter out.
+int ref_strassen(int W, std::size_t m, std::size_t K, std::size_t n, const double* A,
+                 std::size_t lda, const double* B, std::size_t ldb, double* C, std::size_t ldc,
+                 std::size_t cutoff, std::size_t n_min, int variant, unsigned workers) {
+  auto run = [&](auto wc) {
+    constexpr int WW = decltype(wc)::value;
+    return guarded([&] {
+      const auto a = load<WW>(A, m, K, lda);
+      const auto b = load<WW>(B, K, n, ldb);
+      const auto v = static_cast<linalg::KernelVariant>(variant);
+      const auto c = workers > 1 ? linalg::matmul_strassen_parallel(a, b, cutoff, n_min, v, workers)
+                                 : linalg::matmul_strassen(a, b, cutoff, n_min, v);
+      store<WW>(c, C, ldc);
+    });
+  };
+  if (W == 2) return run(std::integral_constant<int, 2>{});
+  if (W == 3) return run(std::integral_constant<int, 3>{});
+  if (W == 4) return run(std::integral_constant<int, 4>{});
+  return 1;
+}
+
+std::uint64_t ref_leaf_multiplies(void) { return linalg::op_counters_read().leaf_multiplies; }
+
 // linalg::ew_apply_into (linalg.hpp:647-684); op: 0 add, 1 mul, 2 add_merge
 int ref_ew(int W, int op, int variant, std::size_t rows, std::size_t cols, const double* a,
            std::size_t lda, const double* b, std::size_t ldb, double* out, std::size_t ldo) {

@@ -63,6 +63,8 @@ _SIGS = {
                                          C.POINTER(MpfkMat), _U64, C.c_int]),
     "mpfk_matmul_naive_into": (C.c_int, [C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat),
                                          C.POINTER(MpfkMat), C.c_int]),
+    "mpfk_matmul_strassen": (C.c_int, [C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat), C.POINTER(MpfkMat), _U64,
+                                       _U64, C.c_int, C.c_uint]),
     "mpfk_last_stats": (C.c_int, [C.POINTER(MpfkStats)]),
     "mpfk_gemm_device": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                    _U64, _P, C.POINTER(C.c_int)]),
@@ -83,6 +85,8 @@ _SIGS = {
     "mpfk_host_alloc": (_P, [_U64]),
     "mpfk_host_free": (None, [_P]),
     "mpfk_fill_baseline": (C.c_int, [C.c_int, C.c_int, _U64, _U64, _U64, _U64, _U64, _P, C.c_int]),
+    "mpfk_fill_random": (C.c_int, [C.c_int, _U64, _U64, _U64, _U64, _P]),
+    "mpfk_gen_paper": (C.c_int, [C.c_int, _U64, _U64, _P, _P]),
     "mpfk_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 

@@ -346,6 +346,9 @@ int enqueue_ew(int W, int op, uint64_t rows, uint64_t cols, double* out, uint64_
     case 14: MPFK_EW(3, kern::EW_ADD_MERGE); break;
     case 16: MPFK_EW(4, kern::EW_ADD); break;
     case 17: MPFK_EW(4, kern::EW_MUL); break;
+    case 11: MPFK_EW(2, kern::EW_SUB); break;
+    case 15: MPFK_EW(3, kern::EW_SUB); break;
+    case 19: MPFK_EW(4, kern::EW_SUB); break;
     default: fail(MPFK_EINVAL, "ew: add_merge is a triple-width operation");
   }
 #undef MPFK_EW
@@ -717,6 +720,25 @@ void renormalize_host(int W, const double* c, double* out) {
   if (arith::nz(eps) && j < W) out[j] = eps;
 }
 
+// rng::random_normalized<W>, random.hpp:54-67: lead in [1, 2), tails at
+// 2^(-53 i) scales, renormalised; redraw the lead if the tail pushed it out.
+void random_normalized(int W, SM64& g, double* out) {
+  double raw[4];
+  raw[0] = 1.0 + g.unit();
+  for (int i = 1; i < W; ++i) {
+    const uint64_t bits = g.next();
+    const double u = static_cast<double>(bits >> 11) * 0x1p-53;
+    raw[i] = ((bits & 1) ? -u : u) * std::ldexp(1.0, -53 * i);
+  }
+  for (int guard = 0; guard < 64; ++guard) {
+    renormalize_host(W, raw, out);
+    if (out[0] >= 1.0 && out[0] < 2.0) return;
+    raw[0] = 1.0 + g.unit();
+  }
+  for (int i = 0; i < W; ++i) out[i] = 0.0;
+  out[0] = 1.0;
+}
+
 void baseline_elem(int W, int wide, SM64& g, double* v) {
   double c[4];
   if (wide) {
@@ -735,6 +757,7 @@ void baseline_elem(int W, int wide, SM64& g, double* v) {
 }
 
 #include "mpfm_io.inl"
+#include "strassen.inl"
 
 }  // namespace
 
@@ -834,6 +857,23 @@ int mpfk_matmul_naive_into(int width, mpfk_mat* C, const mpfk_mat* A, const mpfk
     if (variant < MPFK_NORMAL || variant > MPFK_SIMD_LOADSTORE)
       fail(MPFK_EINVAL, "matmul: unknown kernel variant");
     host_gemm(width, C, A, B, 1);
+  });
+}
+
+int mpfk_matmul_strassen(int width, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B,
+                         uint64_t cutoff, uint64_t n_min, int variant, unsigned workers) {
+  return guarded([&] {
+    check_width(width);
+    check_mat(A, "A");
+    check_mat(B, "B");
+    check_mat(C, "C");
+    // matmul_strassen[_parallel], linalg.hpp:582-605
+    if (A->cols != B->rows) fail(MPFK_EINVAL, "matmul: inner dimensions differ");
+    check_n_min(n_min, variant);
+    if (cutoff < 1) fail(MPFK_EINVAL, "matmul: cutoff must be at least 1");
+    if (workers < 1) fail(MPFK_EINVAL, "matmul: workers must be at least 1");
+    if (C->rows != A->rows || C->cols != B->cols) fail(MPFK_EINVAL, "matmul: result shape mismatch");
+    host_strassen(width, C, A, B, cutoff);
   });
 }
 
@@ -1114,6 +1154,53 @@ int mpfk_fill_baseline(int width, int wide, uint64_t row0, uint64_t rows, uint64
     std::vector<std::thread> th;
     for (unsigned t = 0; t < T; ++t) th.emplace_back(body, t);
     for (auto& x : th) x.join();
+  });
+}
+
+int mpfk_fill_random(int width, uint64_t rows, uint64_t cols, uint64_t stride, uint64_t seed,
+                     double* planes) {
+  return guarded([&] {
+    check_width(width);
+    if (stride < cols) fail(MPFK_EINVAL, "mpfk: stride < cols");
+    if (rows && cols && !planes) fail(MPFK_EINVAL, "mpfk: null planes");
+    SM64 g{seed};
+    const uint64_t ps = rows * stride;
+    std::memset(planes, 0, sizeof(double) * width * ps);
+    for (uint64_t i = 0; i < rows; ++i)
+      for (uint64_t j = 0; j < cols; ++j) {
+        double v[4];
+        random_normalized(width, g, v);
+        for (int w = 0; w < width; ++w) planes[w * ps + i * stride + j] = v[w];
+      }
+  });
+}
+
+int mpfk_gen_paper(int width, uint64_t n, uint64_t stride, double* A, double* B) {
+  return guarded([&] {
+    check_width(width);
+    if (n < 1) fail(MPFK_EINVAL, "gen_paper_matrices: n must be at least 1");
+    if (stride < n) fail(MPFK_EINVAL, "mpfk: stride < cols");
+    const uint64_t ps = n * stride;
+    std::memset(A, 0, sizeof(double) * width * ps);
+    std::memset(B, 0, sizeof(double) * width * ps);
+    double r5[4] = {std::sqrt(5.0), 0, 0, 0}, r3[4] = {std::sqrt(3.0), 0, 0, 0};
+    auto mul = [&](const double* x, const double* y, double* r) {
+      if (width == 2) arith::mp_mul<2>(x, y, r);
+      else if (width == 3) arith::mp_mul<3>(x, y, r);
+      else arith::mp_mul<4>(x, y, r);
+    };
+    for (uint64_t i = 1; i <= n; ++i) {
+      double f[4] = {static_cast<double>(n - i), 0, 0, 0}, brow[4];
+      mul(r3, f, brow);
+      for (uint64_t j = 1; j <= n; ++j) {
+        double gv[4] = {static_cast<double>(i + j - 1), 0, 0, 0}, a[4];
+        mul(r5, gv, a);
+        for (int w = 0; w < width; ++w) {
+          A[w * ps + (i - 1) * stride + (j - 1)] = a[w];
+          B[w * ps + (i - 1) * stride + (j - 1)] = brow[w];
+        }
+      }
+    }
   });
 }
 

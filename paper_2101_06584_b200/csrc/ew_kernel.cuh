@@ -18,7 +18,9 @@ namespace mpfk {
 
 namespace kern {
 
-enum EwOp { EW_ADD = 0, EW_MUL = 1, EW_ADD_MERGE = 2 };  // linalg.hpp:623
+// linalg.hpp:623; EW_SUB is internal (mat_sub of the Strassen plumbing,
+// linalg.hpp:461-470: mpf::sub = add(x, neg(y)), mpf.hpp:267-272)
+enum EwOp { EW_ADD = 0, EW_MUL = 1, EW_ADD_MERGE = 2, EW_SUB = 3 };
 
 struct EwArgs {
   double* out;
@@ -31,7 +33,12 @@ struct EwArgs {
 
 template <int W, int OP>
 __device__ __forceinline__ void ew_one(const double* x, const double* y, double* r) {
-  if constexpr (OP == EW_MUL) arith::mp_mul<W>(x, y, r);
+  if constexpr (OP == EW_SUB) {
+    double ny[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) ny[w] = -y[w];  // exact sign flip (Ops::neg, eft.hpp:126)
+    arith::mp_add<W>(x, ny, r);
+  } else if constexpr (OP == EW_MUL) arith::mp_mul<W>(x, y, r);
   else if constexpr (OP == EW_ADD_MERGE && W == 3) arith::td_add_merge(x, y, r);
   else arith::mp_add<W>(x, y, r);
 }

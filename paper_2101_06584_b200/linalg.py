@@ -364,3 +364,42 @@ def fp64_peak() -> tuple:
 
 def device_count() -> int:
     return N.lib().mpfk_device_count()
+
+
+def fill_random(W: int, rows: int, cols: int, seed: int, pinned: bool = False) -> MPMatrix:
+    """bench::fill_random (bench.cpp:295-302): sequential SplitMix64 stream of
+    rng::random_normalized<W> values (lead in [1, 2))."""
+    m = MPMatrix(W, rows, cols, pinned=pinned)
+    if rows and cols:
+        N.check(N.lib().mpfk_fill_random(W, rows, cols, m.stride(), seed & (2 ** 64 - 1), m.data.ctypes.data))
+    return m
+
+
+def gen_paper_matrices(W: int, n: int):
+    """bench::gen_paper_matrices (bench.cpp:278-292) -> (A, B)."""
+    if n < 1:
+        raise ValueError("gen_paper_matrices: n must be at least 1")
+    A, B = MPMatrix(W, n, n), MPMatrix(W, n, n)
+    N.check(N.lib().mpfk_gen_paper(W, n, A.stride(), A.data.ctypes.data, B.data.ctypes.data))
+    return A, B
+
+
+def matmul_strassen(A: MPMatrix, B: MPMatrix, cutoff: int = 64, n_min: int = 32,
+                    variant: KernelVariant = KernelVariant.NORMAL) -> MPMatrix:
+    """linalg::matmul_strassen (linalg.hpp:582-591) with GPU block leaves."""
+    return matmul_strassen_parallel(A, B, cutoff, n_min, variant, 1)
+
+
+def matmul_strassen_parallel(A: MPMatrix, B: MPMatrix, cutoff: int = 64, n_min: int = 32,
+                             variant: KernelVariant = KernelVariant.NORMAL, workers: int = 1) -> MPMatrix:
+    """linalg::matmul_strassen_parallel (linalg.hpp:596-617); bit-identical to
+    the serial form, as in the reference."""
+    W = _check_same_width(A, B)
+    if cutoff < 0 or n_min < 0 or workers < 0:
+        raise ValueError("matmul: cutoff must be at least 1" if cutoff < 0 else
+                         "matmul: n_min must be at least 1" if n_min < 0 else "matmul: workers must be at least 1")
+    C_ = MPMatrix(W, A.rows(), B.cols())
+    c, a, b = C_._c(), A._c(), B._c()
+    N.check(N.lib().mpfk_matmul_strassen(W, C.byref(c), C.byref(a), C.byref(b), int(cutoff), int(n_min),
+                                         int(variant), int(workers)))
+    return C_
