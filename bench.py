@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--no-overlap", action="store_true",
                     help="N > 1: broadcast all of B before the GEMM instead of K-panel overlap")
     ap.add_argument("--panels", type=int, default=4, help="N > 1: K panels for the overlapped broadcast")
+    ap.add_argument("--dist", action="store_true",
+                    help="initialise the NCCL process group and run the collective path even at N == 1")
+    ap.add_argument("--check", action="store_true",
+                    help="after timing, check the sharded step's C bitwise against a plain one-shot GEMM")
     return ap.parse_args()
 
 
@@ -224,7 +228,8 @@ def run_mpfk(args, ws, rank, local):
     m = k = n
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1 and not dist.is_initialized():
+    use_dist = ws > 1 or args.dist
+    if use_dist and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=dev)
 
     r0, r1 = shard_rows(m, ws, rank)
@@ -245,7 +250,7 @@ def run_mpfk(args, ws, rank, local):
 
     launches = [0]
 
-    overlap = ws > 1 and not args.no_overlap
+    overlap = use_dist and not args.no_overlap
 
     def step():
         ev_mid = torch.cuda.Event(enable_timing=True)
@@ -274,7 +279,7 @@ def run_mpfk(args, ws, rank, local):
     peak_ops, _ = P.fp64_peak()
 
     clocks = ClockSampler(local)
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     clocks.start()
@@ -291,15 +296,22 @@ def run_mpfk(args, ws, rank, local):
         e1.record(stream)
         evs.append((e0, mid, e1))
     torch.cuda.synchronize(dev)
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     clk = clocks.stop()
+    check = None
+    if args.check and rows:
+        ref = torch.zeros_like(dC)
+        P.gemm_device(W, rows, n, k, dA.data_ptr(), ld, rows * ld, dB.data_ptr(), ld, k * ld, ref.data_ptr(), ld,
+                      rows * ld, stream.cuda_stream)
+        torch.cuda.synchronize(dev)
+        check = bool(torch.equal(ref.view(torch.int64), dC.view(torch.int64)))
     step_ms = [a.elapsed_time(c) for a, _, c in evs]
     kern_ms = [b.elapsed_time(c) for _, b, c in evs]
     bc_ms = [a.elapsed_time(b) for a, b, _ in evs]
     t_step = sum(step_ms) / len(step_ms)
     t_kern = sum(kern_ms) / len(kern_ms)
-    if ws > 1:
+    if use_dist:
         t = torch.tensor([t_step, t_kern], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_step, t_kern = t.tolist()
@@ -314,7 +326,7 @@ def run_mpfk(args, ws, rank, local):
         Ch = P.MPMatrix(W, rows, n, pinned=True)
         P.matmul_block_parallel_into(Ch, Ah, Bh2, 32, P.KernelVariant.SIMD_LOADSTORE, 1)  # warm
         e2e_steps = max(1, min(args.steps, 3))
-        if ws > 1:
+        if use_dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
@@ -322,7 +334,7 @@ def run_mpfk(args, ws, rank, local):
             _ = float(Ch.data[0, 0, 0]) if rows else 0.0  # result read on the host
         t_e2e = (time.perf_counter() - t0) / e2e_steps
         st = P.last_stats()
-        if ws > 1:
+        if use_dist:
             t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_e2e = t.item()
@@ -373,7 +385,7 @@ def run_mpfk(args, ws, rank, local):
                        "parallelism": f"row-shard x{ws}" + ((" + NCCL broadcast of B in "
                                                              f"{args.panels} K panels overlapped with the GEMM"
                                                              if overlap else " + NCCL broadcast of B")
-                                                            if ws > 1 else ""),
+                                                            if use_dist else ""),
                        "l2": "flushed between timed steps" if flush is not None else
                              "inputs larger than L2 (126 MB)",
                        "bit_exact": True},
@@ -389,10 +401,12 @@ def run_mpfk(args, ws, rank, local):
             "e2e": e2e,
             "gpu_launches": launches[0],
             "clocks": clk,
-            "bcast_ms": round(sum(bc_ms) / len(bc_ms), 3) if ws > 1 else 0.0,
+            "bcast_ms": round(sum(bc_ms) / len(bc_ms), 3) if (ws > 1 and not overlap) else 0.0,
         }
+        if check is not None:
+            line["check_sharded_equals_one_shot"] = check
         emit(line, args)
-    if ws > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -42,36 +42,21 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
 
 const Entry kEntries[] = {
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),
-    E(2, 64, 64, 16, 4, 4, 2, 1, 16, 2),
-    E(2, 64, 64, 16, 4, 4, 2, 2, 1, 2),
-    E(2, 64, 64, 16, 4, 4, 2, 2, 16, 1),
-    E(2, 64, 64, 16, 4, 4, 3, 2, 16, 2),
-    E(2, 64, 64, 8, 4, 4, 4, 2, 16, 2),
-    E(2, 32, 64, 16, 2, 4, 2, 2, 16, 3),
-    E(2, 32, 64, 16, 2, 4, 2, 2, 16, 4),
-    E(2, 64, 32, 16, 4, 2, 2, 2, 16, 3),
-    E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),
-    E(2, 128, 64, 16, 8, 4, 2, 1, 16, 1),
-    E(2, 64, 128, 16, 4, 8, 2, 1, 16, 1),
-    E(3, 32, 32, 16, 2, 2, 2, 1, 16, 2),
+    E(2, 64, 64, 16, 4, 4, 2, 4, 16, 2),
+    E(2, 64, 64, 16, 4, 4, 2, 8, 16, 2),
+    E(2, 64, 64, 16, 4, 4, 2, 16, 16, 2),
+    E(2, 64, 64, 16, 4, 4, 3, 4, 16, 2),
+    E(2, 32, 32, 16, 2, 2, 2, 4, 16, 4),
     E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),
-    E(3, 32, 32, 16, 2, 2, 2, 1, 1, 3),
-    E(3, 64, 32, 16, 4, 2, 2, 1, 16, 2),
-    E(3, 32, 64, 16, 2, 4, 2, 1, 16, 2),
-    E(3, 32, 32, 16, 2, 2, 3, 1, 16, 3),
-    E(3, 16, 32, 16, 1, 2, 2, 1, 16, 3),
-    E(3, 16, 32, 16, 1, 2, 2, 1, 16, 4),
-    E(3, 64, 64, 16, 4, 4, 2, 1, 16, 1),
-    E(4, 32, 32, 16, 2, 2, 2, 1, 16, 2),
-    E(4, 32, 32, 16, 2, 2, 2, 1, 1, 2),
-    E(4, 32, 32, 16, 2, 2, 2, 1, 16, 1),
-    E(4, 16, 32, 16, 1, 2, 2, 1, 16, 2),
+    E(3, 32, 32, 16, 2, 2, 2, 2, 16, 3),
+    E(3, 32, 32, 16, 2, 2, 2, 4, 16, 3),
+    E(3, 16, 32, 16, 1, 2, 2, 2, 16, 4),
     E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),
-    E(4, 32, 16, 16, 2, 1, 2, 1, 16, 3),
-    E(4, 16, 16, 16, 1, 1, 2, 1, 16, 4),
-    E(4, 32, 32, 16, 2, 2, 3, 1, 16, 2),
-    E(4, 64, 32, 16, 4, 2, 2, 1, 16, 1),
-    E(4, 32, 64, 16, 2, 4, 2, 1, 16, 1),
+    E(4, 16, 32, 16, 1, 2, 2, 2, 16, 3),
+    E(4, 32, 16, 16, 2, 1, 2, 2, 16, 3),
+    E(4, 32, 32, 16, 2, 2, 2, 2, 16, 2),
+    E(4, 16, 16, 16, 1, 1, 2, 2, 16, 4),
+    E(4, 16, 64, 16, 1, 4, 2, 1, 16, 2),
 };
 }  // namespace
 

@@ -31,7 +31,7 @@ def shard_rows(m: int, world: int, rank: int, align: int = 64):
 def replicate_b(dB, src: int = 0, group=None):
     """B from the root rank to all ranks (NCCL broadcast on GPU tensors)."""
     import torch.distributed as dist
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_initialized():
         dist.broadcast(dB, src=src, group=group)
     return dB
 
@@ -77,7 +77,7 @@ def sharded_gemm_step_overlapped(W: int, dA, dB, dC, rows: int, n: int, k: int, 
     the device kernel (the CPU tests pass the oracle)."""
     import torch.distributed as dist
     parts = k_panels(k, panels)
-    multi = dist.is_initialized() and dist.get_world_size(group) > 1
+    multi = dist.is_initialized()  # (a world of one still runs the collective path)
     works = []
     if multi:
         for k0, k1 in parts:
