@@ -118,6 +118,11 @@ struct Device {
 };
 
 std::mutex g_mu;
+// Host-buffer calls share each device's grow-only operand buffers, streams
+// and events; they are serialised (each call is synchronous, like the
+// reference's).  Device-resident entry points run on the caller's stream and
+// take no lock.
+std::mutex g_call_mu;
 std::vector<Device> g_dev;
 int g_ndev = -1;
 
@@ -416,6 +421,7 @@ struct Shard {
 // The multi-GPU host-buffer GEMM.  Device layout: planes packed with
 // ld = pad4(cols) (16-byte rows for cp.async), A shard rows only, full B.
 void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigned gpus) {
+  std::lock_guard<std::mutex> call_lock(g_call_mu);
   const auto t0 = std::chrono::steady_clock::now();
   const uint64_t m = A->rows, K = A->cols, n = B->cols;
   mpfk_stats st{};
@@ -919,6 +925,7 @@ int mpfk_ew_apply_into(int width, int op, mpfk_mat* out, const mpfk_mat* a, cons
     if (op == kern::EW_ADD_MERGE && width != 3)
       fail(MPFK_EINVAL, "ew: add_merge is a triple-width operation");
     const uint64_t rows = a->rows, cols = a->cols;
+    std::lock_guard<std::mutex> call_lock(g_call_mu);
     mpfk_stats st{};
     const auto t0 = std::chrono::steady_clock::now();
     if (rows && cols) {

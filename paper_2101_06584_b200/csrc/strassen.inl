@@ -126,6 +126,7 @@ struct StrassenCtx {
 // download C.  `workers` only validates (the seven products are
 // independent; the reference's parallel form is bit-identical to serial).
 void host_strassen(int W, mpfk_mat* Cm, const mpfk_mat* A, const mpfk_mat* B, uint64_t cutoff) {
+  std::lock_guard<std::mutex> call_lock(g_call_mu);
   const auto t0 = std::chrono::steady_clock::now();
   mpfk_stats st{};
   const uint64_t m = A->rows, K = A->cols, n = B->cols;
