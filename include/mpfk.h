@@ -116,6 +116,13 @@ int mpfk_matmul_naive_into(int width, mpfk_mat *C, const mpfk_mat *A, const mpfk
  * leaf's count_matmul, like linalg.hpp:457, :468, :570. */
 int mpfk_matmul_strassen(int width, mpfk_mat *C, const mpfk_mat *A, const mpfk_mat *B,
                          uint64_t cutoff, uint64_t n_min, int variant, unsigned workers);
+/* Device-resident Strassen (same recursion and bits) on the current device /
+ * `stream`: level-synchronous, one batched block GEMM for all leaves.
+ * Scratch comes from the stream-ordered allocator. */
+int mpfk_strassen_device(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                         uint64_t lda, uint64_t a_plane, const double *B, uint64_t ldb,
+                         uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane,
+                         uint64_t cutoff, void *stream, int *launches);
 int mpfk_last_stats(mpfk_stats *out);
 
 /* ---- GEMM, device-resident operands ------------------------------------ */

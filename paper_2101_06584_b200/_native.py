@@ -65,6 +65,8 @@ _SIGS = {
                                          C.POINTER(MpfkMat), C.c_int]),
     "mpfk_matmul_strassen": (C.c_int, [C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat), C.POINTER(MpfkMat), _U64,
                                        _U64, C.c_int, C.c_uint]),
+    "mpfk_strassen_device": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
+                                       _U64, _U64, _P, C.POINTER(C.c_int)]),
     "mpfk_last_stats": (C.c_int, [C.POINTER(MpfkStats)]),
     "mpfk_gemm_device": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                    _U64, _P, C.POINTER(C.c_int)]),

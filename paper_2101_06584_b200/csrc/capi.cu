@@ -26,6 +26,7 @@
 #include "../../include/mpfk.h"
 #include "ew_kernel.cuh"
 #include "gemm_kernel.cuh"
+#include "strassen_kernels.cuh"
 #include "mpf_arith.cuh"
 
 namespace {
@@ -254,7 +255,7 @@ void configure_once() {
 
 template <class Cfg>
 long long tiles_of(const kern::GemmArgs& g) {
-  return (long long)((g.N + Cfg::BN - 1) / Cfg::BN) * ((g.M + Cfg::BM - 1) / Cfg::BM);
+  return (long long)((g.N + Cfg::BN - 1) / Cfg::BN) * ((g.M + Cfg::BM - 1) / Cfg::BM) * std::max(g.batch, 1);
 }
 
 // Expected fraction of FP64 peak: steady-state efficiency of the tile shape
@@ -291,6 +292,8 @@ __global__ void zero_planes_kernel(double* C, long long ldc, long long pc, int M
 }
 
 // Enqueue C = A*B on the current device.  Returns kernel launches.
+int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s);
+
 // accumulate: continue the chains already in C over this K panel (see
 // GemmArgs::accumulate); k == 0 is then a no-op.
 int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
@@ -312,6 +315,30 @@ int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uin
   g.pa = (long long)pa, g.pb = (long long)pb, g.pc = (long long)pc;
   g.M = (int)m, g.N = (int)n, g.K = (int)k;
   g.accumulate = accumulate ? 1 : 0;
+  g.batch = 1, g.sa = g.sb = g.sc = 0;
+  return dispatch_gemm(W, g, s);
+}
+
+// A strided batch of `batch` products of one shape (Strassen leaves).
+int enqueue_gemm_batched(int W, int batch, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                         uint64_t pa, uint64_t sa, const double* B, uint64_t ldb, uint64_t pb, uint64_t sb,
+                         double* C, uint64_t ldc, uint64_t pc, uint64_t sc, cudaStream_t s) {
+  if (batch <= 0 || m == 0 || n == 0) return 0;
+  if (k == 0) {
+    for (int b = 0; b < batch; ++b) enqueue_gemm(W, m, n, 0, A, lda, pa, B, ldb, pb, C + b * sc, ldc, pc, s);
+    return batch;
+  }
+  kern::GemmArgs g;
+  g.A = A, g.B = B, g.C = C;
+  g.lda = (long long)lda, g.ldb = (long long)ldb, g.ldc = (long long)ldc;
+  g.pa = (long long)pa, g.pb = (long long)pb, g.pc = (long long)pc;
+  g.M = (int)m, g.N = (int)n, g.K = (int)k;
+  g.accumulate = 0;
+  g.batch = batch, g.sa = (long long)sa, g.sb = (long long)sb, g.sc = (long long)sc;
+  return dispatch_gemm(W, g, s);
+}
+
+int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s) {
   switch (W) {
     case 2:
       if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
@@ -880,6 +907,26 @@ int mpfk_matmul_strassen(int width, mpfk_mat* C, const mpfk_mat* A, const mpfk_m
     if (workers < 1) fail(MPFK_EINVAL, "matmul: workers must be at least 1");
     if (C->rows != A->rows || C->cols != B->cols) fail(MPFK_EINVAL, "matmul: result shape mismatch");
     host_strassen(width, C, A, B, cutoff);
+  });
+}
+
+int mpfk_strassen_device(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                         uint64_t a_plane, const double* B, uint64_t ldb, uint64_t b_plane, double* C,
+                         uint64_t ldc, uint64_t c_plane, uint64_t cutoff, void* stream, int* launches) {
+  return guarded([&] {
+    check_width(width);
+    if (cutoff < 1) fail(MPFK_EINVAL, "matmul: cutoff must be at least 1");
+    if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
+    if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
+      fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+         reinterpret_cast<uintptr_t>(C)) & 15)
+      fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    const int l = strassen_device(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, cutoff,
+                                  static_cast<cudaStream_t>(stream));
+    if (launches) *launches = l;
   });
 }
 

@@ -40,6 +40,10 @@ struct GemmArgs {
   // (QuadRow::axpy reloads C, linalg.hpp:261), so splitting K into panels
   // and continuing from C is bit-identical.
   int accumulate;
+  // Strided batch of independent products (the Strassen leaves, all of one
+  // shape): matrix b of A/B/C starts sa/sb/sc doubles after matrix b-1.
+  int batch;
+  long long sa, sb, sc;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -119,7 +123,7 @@ __device__ __forceinline__ void tile_coords(int lin, int tiles_m, int tiles_n, i
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
-    mpgemm_kernel(const GemmArgs g) {
+    mpgemm_kernel(const GemmArgs g0) {
   constexpr int W = Cfg::W, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, TX = Cfg::TX, TY = Cfg::TY;
   constexpr int STAGES = Cfg::STAGES;
@@ -128,8 +132,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   double* Bs0 = smem + STAGES * Cfg::A_STAGE;
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const int tiles_m = (g0.M + BM - 1) / BM, tiles_n = (g0.N + BN - 1) / BN;
+  int lin = blockIdx.x, bz = 0;
+  if (g0.batch > 1) {
+    bz = lin / (tiles_m * tiles_n);
+    lin -= bz * tiles_m * tiles_n;
+  }
+  GemmArgs g = g0;
+  g.A += bz * g0.sa;
+  g.B += bz * g0.sb;
+  g.C += bz * g0.sc;
   int tile_m, tile_n;
-  tile_coords<Cfg::GROUP_M>(blockIdx.x, (g.M + BM - 1) / BM, (g.N + BN - 1) / BN, tile_m, tile_n);
+  tile_coords<Cfg::GROUP_M>(lin, tiles_m, tiles_n, tile_m, tile_n);
   const int m0 = tile_m * BM, n0 = tile_n * BN;
   const int ktiles = (g.K + BK - 1) / BK;
 

@@ -2,135 +2,172 @@
 // leaf.  Included by capi.cu inside its anonymous
 // namespace.
 //
-// Restates linalg.hpp:472-617 step for step on device-resident operands:
-// per-level zero padding to even sizes (copy_block, :483-498), the 14
-// operands in the fixed M1..M7 order (:522-540) built with the width's exact
-// add / sub (mat_add/mat_sub, :450-470 -> the ew kernel), the seven products
-// recursed until min(m, K, n) <= cutoff where the leaf is the block GEMM
-// (:569-571), and the combine (:543-563) with clipping paste.  Every step is
-// the reference's operation on the same values in the same order, so the
-// result is bit-identical to mpfkit::linalg::matmul_strassen (and to its
-// parallel form, which only reorders independent products).  Op counters
-// follow the reference: mat_add/mat_sub add rows*cols adds, each leaf adds
-// one leaf multiply plus count_matmul of its block GEMM.
+// The reference recurses depth-first (linalg.hpp:565-578), one node at a
+// time.  All nodes at one depth have the same padded shape (ceil halves of
+// their parent's), so here a whole level runs at once:
+//   level d (batch b = 7^d): one strassen_operands launch per side builds
+//   all 7b child operands; the next level recurses on them; at the leaf depth
+//   (min(m, K, n) <= cutoff) ONE batched GEMM launch computes all 7^D leaf
+//   products; on the way back one strassen_combine launch per level builds
+//   every parent's C from its children's products.
+// A few dozen launches instead of ~10^4.  If a level's operands would not
+// fit the memory budget, that level is processed depth-first (children one
+// at a time) and the levels below it level-synchronously again.
+// Each element sees the reference's operations in the reference's order, so
+// the result is bit-identical to mpfkit::linalg::matmul_strassen (and its
+// parallel form).  Op counters follow the reference: every mat_add/mat_sub
+// adds rows*cols adds (linalg.hpp:457, 468), every leaf one leaf multiply
+// (:570) plus count_matmul of its block GEMM (:387).
 
-struct DMat {
+struct BMat {  // a batch of width-W device matrices
   double* p = nullptr;
-  uint64_t rows = 0, cols = 0, ld = 0;
-  uint64_t plane() const { return rows * ld; }
+  uint64_t rows = 0, cols = 0, ld = 0, plane = 0, bstride = 0;
+  int batch = 0;
+  kern::BatchRef ref() const {
+    return {p, (long long)ld, (long long)plane, (long long)bstride};
+  }
+  kern::BatchOut out() const { return {p, (long long)ld, (long long)plane, (long long)bstride}; }
 };
 
 struct StrassenCtx {
   int W;
   uint64_t cutoff;
   cudaStream_t s;
-  std::vector<double*> owned;  // freed stream-ordered at the end of each level
+  uint64_t budget;  // bytes the level-synchronous scratch may use
+  int launches = 0;
 
-  DMat alloc(uint64_t rows, uint64_t cols) {
-    DMat m;
+  BMat alloc(int batch, uint64_t rows, uint64_t cols) {
+    BMat m;
     m.rows = rows, m.cols = cols, m.ld = std::max<uint64_t>(pad4(cols), 4);
-    const size_t bytes = sizeof(double) * W * std::max<uint64_t>(m.plane(), 1);
+    m.plane = rows * m.ld, m.bstride = W * m.plane, m.batch = batch;
+    const size_t bytes = sizeof(double) * std::max<uint64_t>(uint64_t(batch) * m.bstride, 1);
     ck(cudaMallocAsync(reinterpret_cast<void**>(&m.p), bytes, s), "cudaMallocAsync");
-    ck(cudaMemsetAsync(m.p, 0, bytes, s), "cudaMemsetAsync");
     return m;
   }
-  void release(DMat& m) {
+  void release(BMat& m) {
     if (m.p) ck(cudaFreeAsync(m.p, s), "cudaFreeAsync");
     m.p = nullptr;
   }
-
-  // copy_block, linalg.hpp:483-498: window outside the source stays +0
-  DMat copy_block(const DMat& src, uint64_t i0, uint64_t j0, uint64_t rows, uint64_t cols) {
-    DMat r = alloc(rows, cols);
-    if (i0 >= src.rows || j0 >= src.cols) return r;
-    const uint64_t ni = std::min(rows, src.rows - i0), nj = std::min(cols, src.cols - j0);
-    for (int w = 0; w < W; ++w)
-      ck(cudaMemcpy2DAsync(r.p + w * r.plane(), r.ld * 8, src.p + w * src.plane() + i0 * src.ld + j0,
-                           src.ld * 8, nj * 8, ni, cudaMemcpyDeviceToDevice, s),
-         "copy_block");
-    return r;
+  uint64_t bytes_of(uint64_t batch, uint64_t rows, uint64_t cols) const {
+    return 8ull * W * batch * rows * std::max<uint64_t>(pad4(cols), 4);
+  }
+  // scratch a level-synchronous subtree needs below a node batch
+  uint64_t subtree_bytes(uint64_t batch, uint64_t m, uint64_t K, uint64_t n) const {
+    if (std::min({m, K, n}) <= cutoff) return 0;
+    const uint64_t hm = (m + 1) / 2, hk = (K + 1) / 2, hn = (n + 1) / 2, c = batch * 7;
+    return bytes_of(c, hm, hk) + bytes_of(c, hk, hn) + bytes_of(c, hm, hn) + subtree_bytes(c, hm, hk, hn);
   }
 
-  // paste_block, linalg.hpp:501-514: clipped to dst's bounds
-  void paste_block(DMat& dst, const DMat& src, uint64_t i0, uint64_t j0) {
-    if (i0 >= dst.rows || j0 >= dst.cols) return;
-    const uint64_t ni = std::min(src.rows, dst.rows - i0), nj = std::min(src.cols, dst.cols - j0);
-    for (int w = 0; w < W; ++w)
-      ck(cudaMemcpy2DAsync(dst.p + w * dst.plane() + i0 * dst.ld + j0, dst.ld * 8, src.p + w * src.plane(),
-                           src.ld * 8, nj * 8, ni, cudaMemcpyDeviceToDevice, s),
-         "paste_block");
+  unsigned grid_for(uint64_t elems) const {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((elems + 255) / 256, 148ull * 16));
   }
 
-  // mat_add / mat_sub, linalg.hpp:450-470
-  DMat ew(const DMat& a, const DMat& b, int op) {
-    DMat r = alloc(a.rows, a.cols);
-    enqueue_ew(W, op, a.rows, a.cols, r.p, r.ld, r.plane(), a.p, a.ld, a.plane(), b.p, b.ld, b.plane(), s);
-    g_adds.fetch_add(a.rows * a.cols, std::memory_order_relaxed);
-    return r;
+  template <int SIDE>
+  void operands(const BMat& src, const BMat& dst, uint64_t h0, uint64_t h1, int t0, int t1) {
+    const uint64_t elems = uint64_t(src.batch) * h0 * h1;
+    const unsigned g = grid_for(elems);
+#define MPFK_OPS(WW)                                                                               \
+  kern::strassen_operands<WW, SIDE><<<g, 256, 0, s>>>(src.ref(), dst.out(), src.batch, (int)src.rows, \
+                                                      (int)src.cols, (int)h0, (int)h1, t0, t1)
+    if (W == 2) MPFK_OPS(2);
+    else if (W == 3) MPFK_OPS(3);
+    else MPFK_OPS(4);
+#undef MPFK_OPS
+    ck(cudaGetLastError(), "strassen operands launch");
+    ++launches;
+    // mat_add/mat_sub among the 7 (L: t in {0,1,4,5,6}; R: t in {0,2,3,5,6})
+    uint64_t ops = 0;
+    for (int t = t0; t < t1; ++t) ops += SIDE == 0 ? (t != 2 && t != 3) : (t != 1 && t != 4);
+    g_adds.fetch_add(ops * src.batch * h0 * h1, std::memory_order_relaxed);
   }
-  DMat add(const DMat& a, const DMat& b) { return ew(a, b, kern::EW_ADD); }
-  DMat sub(const DMat& a, const DMat& b) { return ew(a, b, kern::EW_SUB); }
-  DMat copy(const DMat& a) { return copy_block(a, 0, 0, a.rows, a.cols); }
 
-  // strassen_rec, linalg.hpp:565-578
-  DMat rec(const DMat& A, const DMat& B, int& launches) {
-    const uint64_t m = A.rows, K = A.cols, n = B.cols;
-    if (std::min({m, K, n}) <= cutoff) {
-      g_leaf.fetch_add(1, std::memory_order_relaxed);
-      DMat C = alloc(m, n);
-      launches += enqueue_gemm(W, m, n, K, A.p, A.ld, A.plane(), B.p, B.ld, B.plane(), C.p, C.ld,
-                               C.plane(), s);
-      count_matmul(m, n, K);
-      return C;
+  void combine(const BMat& M, const BMat& C) {
+    const uint64_t elems = uint64_t(C.batch) * C.rows * C.cols;
+    const unsigned g = grid_for(elems);
+#define MPFK_CMB(WW) \
+  kern::strassen_combine<WW><<<g, 256, 0, s>>>(M.ref(), C.out(), C.batch, (int)C.rows, (int)C.cols, (int)M.rows, (int)M.cols)
+    if (W == 2) MPFK_CMB(2);
+    else if (W == 3) MPFK_CMB(3);
+    else MPFK_CMB(4);
+#undef MPFK_CMB
+    ck(cudaGetLastError(), "strassen combine launch");
+    ++launches;
+    g_adds.fetch_add(8ull * C.batch * M.rows * M.cols, std::memory_order_relaxed);  // 8 adds/subs
+  }
+
+  // L: batch of m x K, R: batch of K x n; writes the products into C
+  // (batch of m x n, possibly a strided view of a larger buffer).
+  void solve(const BMat& L, const BMat& R, const BMat& C) {
+    const uint64_t m = L.rows, K = L.cols, n = R.cols;
+    const int b = L.batch;
+    if (std::min({m, K, n}) <= cutoff) {  // the leaves: one batched block GEMM
+      g_leaf.fetch_add(b, std::memory_order_relaxed);
+      launches += enqueue_gemm_batched(W, b, m, n, K, L.p, L.ld, L.plane, L.bstride, R.p, R.ld, R.plane,
+                                       R.bstride, C.p, C.ld, C.plane, C.bstride, s);
+      if (K) {
+        g_muls.fetch_add(uint64_t(b) * m * n * K, std::memory_order_relaxed);
+        g_adds.fetch_add(uint64_t(b) * m * n * (K - 1), std::memory_order_relaxed);
+      }
+      return;
     }
     const uint64_t hm = (m + 1) / 2, hk = (K + 1) / 2, hn = (n + 1) / 2;
-    DMat A11 = copy_block(A, 0, 0, hm, hk), A12 = copy_block(A, 0, hk, hm, hk);
-    DMat A21 = copy_block(A, hm, 0, hm, hk), A22 = copy_block(A, hm, hk, hm, hk);
-    DMat B11 = copy_block(B, 0, 0, hk, hn), B12 = copy_block(B, 0, hn, hk, hn);
-    DMat B21 = copy_block(B, hk, 0, hk, hn), B22 = copy_block(B, hk, hn, hk, hn);
-    // the 14 operands in the fixed M1..M7 order, linalg.hpp:532-538
-    DMat L[7], R[7];
-    L[0] = add(A11, A22), R[0] = add(B11, B22);  // M1
-    L[1] = add(A21, A22), R[1] = copy(B11);      // M2
-    L[2] = copy(A11), R[2] = sub(B12, B22);      // M3
-    L[3] = copy(A22), R[3] = sub(B21, B11);      // M4
-    L[4] = add(A11, A12), R[4] = copy(B22);      // M5
-    L[5] = sub(A21, A11), R[5] = add(B11, B12);  // M6
-    L[6] = sub(A12, A22), R[6] = add(B21, B22);  // M7
-    for (DMat* x : {&A11, &A12, &A21, &A22, &B11, &B12, &B21, &B22}) release(*x);
-    DMat M[7];
-    for (int t = 0; t < 7; ++t) {
-      M[t] = rec(L[t], R[t], launches);
-      release(L[t]);
-      release(R[t]);
+    BMat M = alloc(b * 7, hm, hn);
+    if (subtree_bytes(b, m, K, n) <= budget) {
+      BMat L2 = alloc(b * 7, hm, hk), R2 = alloc(b * 7, hk, hn);
+      operands<0>(L, L2, hm, hk, 0, 7);
+      operands<1>(R, R2, hk, hn, 0, 7);
+      solve(L2, R2, M);
+      release(L2);
+      release(R2);
+    } else {  // depth-first over the 7 products of this level
+      for (int t = 0; t < 7; ++t) {
+        BMat L2 = alloc(b, hm, hk), R2 = alloc(b, hk, hn);
+        operands<0>(L, L2, hm, hk, t, t + 1);
+        operands<1>(R, R2, hk, hn, t, t + 1);
+        BMat Mt = M;  // children b*7 + t: a strided view
+        Mt.p = M.p + t * M.bstride;
+        Mt.bstride = 7 * M.bstride;
+        Mt.batch = b;
+        solve(L2, R2, Mt);
+        release(L2);
+        release(R2);
+      }
     }
-    // strassen_combine, linalg.hpp:543-563
-    DMat t1 = add(M[0], M[3]), t2 = sub(t1, M[4]);
-    DMat C11 = add(t2, M[6]);
-    DMat C12 = add(M[2], M[4]);
-    DMat C21 = add(M[1], M[3]);
-    DMat t3 = sub(M[0], M[1]), t4 = add(t3, M[2]);
-    DMat C22 = add(t4, M[5]);
-    DMat C = alloc(m, n);
-    paste_block(C, C11, 0, 0);
-    paste_block(C, C12, 0, hn);
-    paste_block(C, C21, hm, 0);
-    paste_block(C, C22, hm, hn);
-    for (DMat* x : {&t1, &t2, &t3, &t4, &C11, &C12, &C21, &C22}) release(*x);
-    for (auto& x : M) release(x);
-    return C;
+    combine(M, C);
+    release(M);
   }
 };
 
-// Host-buffer matmul_strassen: upload A and B, recurse on the device,
-// download C.  `workers` only validates (the seven products are
-// independent; the reference's parallel form is bit-identical to serial).
+// Strassen on device operands (single matrices) of the current device.
+int strassen_device(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda, uint64_t pa,
+                    const double* B, uint64_t ldb, uint64_t pb, double* C, uint64_t ldc, uint64_t pc,
+                    uint64_t cutoff, cudaStream_t s) {
+  size_t free_b = 0, total_b = 0;
+  ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  uint64_t budget = (uint64_t)(0.4 * free_b);
+  if (const char* e = std::getenv("MPFK_STRASSEN_BUDGET_BYTES")) budget = std::strtoull(e, nullptr, 10);
+  StrassenCtx ctx{W, cutoff, s, budget};
+  BMat a, b, c;
+  a.p = const_cast<double*>(A), a.rows = m, a.cols = k, a.ld = lda, a.plane = pa, a.bstride = W * pa, a.batch = 1;
+  b.p = const_cast<double*>(B), b.rows = k, b.cols = n, b.ld = ldb, b.plane = pb, b.bstride = W * pb, b.batch = 1;
+  c.p = C, c.rows = m, c.cols = n, c.ld = ldc, c.plane = pc, c.bstride = W * pc, c.batch = 1;
+  if (m == 0 || n == 0) {
+    g_leaf.fetch_add(1, std::memory_order_relaxed);  // min(m, K, n) <= cutoff: one empty leaf
+    return 0;
+  }
+  ctx.solve(a, b, c);
+  return ctx.launches;
+}
+
+// Host-buffer matmul_strassen: upload A and B, run on the device, download C.
+// `workers` only validates (the reference's parallel form reorders
+// independent products and is bit-identical to serial).
 void host_strassen(int W, mpfk_mat* Cm, const mpfk_mat* A, const mpfk_mat* B, uint64_t cutoff) {
   std::lock_guard<std::mutex> call_lock(g_call_mu);
   const auto t0 = std::chrono::steady_clock::now();
   mpfk_stats st{};
   const uint64_t m = A->rows, K = A->cols, n = B->cols;
-  if (m == 0 || n == 0) {  // min(m, K, n) <= cutoff: one (empty) leaf
+  if (m == 0 || n == 0) {
     g_leaf.fetch_add(1, std::memory_order_relaxed);
     zero_host_pads(W, Cm);
     t_stats = st;
@@ -139,37 +176,28 @@ void host_strassen(int W, mpfk_mat* Cm, const mpfk_mat* A, const mpfk_mat* B, ui
   const int dev = current_device();
   ensure_devices(1, dev);
   Device& D = g_dev[dev];
-  StrassenCtx ctx{W, cutoff, D.stream, {}};
-  ck(cudaEventRecord(D.ev[0], D.stream), "event");
-  DMat dA = ctx.alloc(m, K), dB = ctx.alloc(K, n);
+  const uint64_t lda = pad4(K), ldb = pad4(n), ldc = pad4(n);
+  grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(m * lda, 1));
+  grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
+  grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(m * ldc, 1));
   const uint64_t pa = plane_of(A), pb = plane_of(B), pc = plane_of(Cm);
-  for (int w = 0; w < W; ++w) {
+  ck(cudaEventRecord(D.ev[0], D.stream), "event");
+  for (int w = 0; w < W; ++w)
     if (K) {
-      ck(cudaMemcpy2DAsync(dA.p + w * dA.plane(), dA.ld * 8, A->base + w * pa, A->stride * 8, K * 8, m,
+      ck(cudaMemcpy2DAsync(D.dA + w * m * lda, lda * 8, A->base + w * pa, A->stride * 8, K * 8, m,
                            cudaMemcpyHostToDevice, D.stream), "H2D A");
-      ck(cudaMemcpy2DAsync(dB.p + w * dB.plane(), dB.ld * 8, B->base + w * pb, B->stride * 8, n * 8, K,
+      ck(cudaMemcpy2DAsync(D.dB + w * K * ldb, ldb * 8, B->base + w * pb, B->stride * 8, n * 8, K,
                            cudaMemcpyHostToDevice, D.stream), "H2D B");
     }
-  }
   ck(cudaEventRecord(D.ev[1], D.stream), "event");
-  int launches = 0;
-  DMat dC;
-  if (K == 0) {
-    dC = ctx.alloc(m, n);  // an empty product: every cell +0
-    g_leaf.fetch_add(1, std::memory_order_relaxed);
-  } else {
-    dC = ctx.rec(dA, dB, launches);
-  }
+  st.kernel_launches = strassen_device(W, m, n, K, D.dA, lda, m * lda, D.dB, ldb, K * ldb, D.dC, ldc,
+                                       m * ldc, cutoff, D.stream);
   ck(cudaEventRecord(D.ev[2], D.stream), "event");
   for (int w = 0; w < W; ++w)
-    ck(cudaMemcpy2DAsync(Cm->base + w * pc, Cm->stride * 8, dC.p + w * dC.plane(), dC.ld * 8, n * 8, m,
+    ck(cudaMemcpy2DAsync(Cm->base + w * pc, Cm->stride * 8, D.dC + w * m * ldc, ldc * 8, n * 8, m,
                          cudaMemcpyDeviceToHost, D.stream), "D2H C");
   ck(cudaEventRecord(D.ev[3], D.stream), "event");
-  ctx.release(dA);
-  ctx.release(dB);
-  ctx.release(dC);
   ck(cudaEventSynchronize(D.ev[3]), "Strassen execution");
-  ck(cudaStreamSynchronize(D.stream), "Strassen execution");
   zero_host_pads(W, Cm);
   float x = 0;
   cudaEventElapsedTime(&x, D.ev[0], D.ev[1]);
@@ -178,7 +206,6 @@ void host_strassen(int W, mpfk_mat* Cm, const mpfk_mat* A, const mpfk_mat* B, ui
   st.kernel_ms = x;
   cudaEventElapsedTime(&x, D.ev[2], D.ev[3]);
   st.d2h_ms = x;
-  st.kernel_launches = launches;
   st.n_gpus = 1;
   st.h2d_bytes = 8ull * W * (m * K + K * n);
   st.d2h_bytes = 8ull * W * m * n;

@@ -72,6 +72,7 @@ int tune_run(int i, int M, int N, int K, const double* A, long long lda, long lo
   g.lda = lda, g.ldb = ldb, g.ldc = ldc, g.pa = pa, g.pb = pb, g.pc = pc;
   g.M = M, g.N = N, g.K = K;
   g.accumulate = 0;
+  g.batch = 1, g.sa = g.sb = g.sc = 0;
   return (int)kEntries[i].run(g, (cudaStream_t)stream);
 }
 }

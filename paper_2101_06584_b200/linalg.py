@@ -403,3 +403,12 @@ def matmul_strassen_parallel(A: MPMatrix, B: MPMatrix, cutoff: int = 64, n_min: 
     N.check(N.lib().mpfk_matmul_strassen(W, C.byref(c), C.byref(a), C.byref(b), int(cutoff), int(n_min),
                                          int(variant), int(workers)))
     return C_
+
+
+def strassen_device(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int, ldb: int,
+                    b_plane: int, C_ptr: int, ldc: int, c_plane: int, cutoff: int = 64, stream: int = 0) -> int:
+    """Device-resident Strassen (mpfk_strassen_device); returns kernel launches."""
+    launches = C.c_int(0)
+    N.check(N.lib().mpfk_strassen_device(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc, c_plane,
+                                         cutoff, stream or None, C.byref(launches)))
+    return launches.value

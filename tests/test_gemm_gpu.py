@@ -245,3 +245,15 @@ def test_k_panel_continuation_bitwise(gpu_lib, W):
           dC.data_ptr(), ldb, m * ldb)
     torch.cuda.synchronize()
     assert mismatches(dC.cpu().numpy(), O.ref_gemm(A, B, k, n)) == 0
+
+
+@pytest.mark.parametrize("W", WIDTHS)
+@pytest.mark.parametrize("scale", [-520, -560, 480])
+def test_extreme_magnitudes_bitwise(gpu_lib, W, scale):
+    """Products in the subnormal range (two_prod's error term underflows,
+    eft.hpp:61-62) and near the top of the exponent range: both sides follow
+    IEEE binary64 without flush-to-zero, so the bits must still agree."""
+    n = 24
+    A = random_signed(W, n, n, 700 + W) * np.ldexp(1.0, scale)
+    B = random_signed(W, n, n, 710 + W) * np.ldexp(1.0, scale if scale < 0 else 20)
+    check_vs_reference(gpu_lib, A, B, n, n)

@@ -78,3 +78,35 @@ def test_strassen_odd_padding_accuracy_and_errors(gpu_lib):
         P.matmul_strassen_parallel(x, x, 64, 32, P.KernelVariant.SIMD_SET, 0)
     with pytest.raises(ValueError, match="matmul: inner dimensions differ"):
         P.matmul_strassen(x, P.MPMatrix(2, 31, 32))
+
+
+def test_strassen_depth_first_fallback_bitwise(gpu_lib, monkeypatch):
+    """With no scratch budget every level runs depth-first (children one at a
+    time, strided product views); the bits and counters must not change."""
+    P = gpu_lib
+    A = random_signed(4, 37, 41, 900)
+    B = random_signed(4, 41, 29, 901)
+    want = O.ref_strassen(A, B, 41, 29, cutoff=6, n_min=4)
+    P.op_counters_reset()
+    fast = P.matmul_strassen(to_mp(A, 41), to_mp(B, 29), 6, 4)
+    c_fast = P.op_counters_read()
+    monkeypatch.setenv("MPFK_STRASSEN_BUDGET_BYTES", "1")
+    P.op_counters_reset()
+    slow = P.matmul_strassen(to_mp(A, 41), to_mp(B, 29), 6, 4)
+    assert P.op_counters_read() == c_fast
+    assert mismatches(fast.data, want) == 0 and mismatches(slow.data, want) == 0
+
+
+def test_strassen_device_entry(gpu_lib):
+    import torch
+    P = gpu_lib
+    W, m, k, n = 2, 130, 96, 70
+    A = random_signed(W, m, k, 910)
+    B = random_signed(W, k, n, 911)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dC = torch.zeros((W, m, B.shape[2]), dtype=torch.float64, device="cuda")
+    launches = P.strassen_device(W, m, n, k, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), B.shape[2],
+                                 k * B.shape[2], dC.data_ptr(), B.shape[2], m * B.shape[2], cutoff=16)
+    torch.cuda.synchronize()
+    assert launches < 20  # level-synchronous: a handful of launches, not 7^depth
+    assert mismatches(dC.cpu().numpy(), O.ref_strassen(A, B, k, n, cutoff=16, n_min=4)) == 0
