@@ -197,6 +197,14 @@ void ensure_devices(int n, int first = 0) {
     for (auto& e : D.ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     for (auto& e : D.evA) ck(cudaEventCreate(&e), "cudaEventCreate");
     for (auto& e : D.evC) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    // keep stream-ordered scratch (Strassen levels) mapped between calls
+    // instead of returning it to the OS at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+      uint64_t keep = ~uint64_t(0);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
     D.ready = true;
   }
   cudaSetDevice(prev);
