@@ -8,8 +8,10 @@
 //
 // Every entry point only marshals plain SoA arrays into mpfkit types and
 // calls the reference's public API:
-//   ref_gemm        -> mpfkit::linalg::matmul_block_parallel_into (linalg.hpp:402-433)
-//   ref_gemm_naive  -> mpfkit::linalg::matmul_naive_into          (linalg.hpp:346-358)
+//   ref_gemm        -> mpfkit::linalg::matmul_block_parallel_into (linalg.hpp:402-433),
+//                      or matmul_naive_into (linalg.hpp:346-358) with naive != 0
+//   ref_strassen    -> matmul_strassen[_parallel]                  (linalg.hpp:582-617)
+//   ref_ew          -> linalg::ew_apply_into                       (linalg.hpp:647-684)
 //   ref_add/ref_mul -> mpfkit::mpf::add/mul<W>                    (mpf.hpp:341-353)
 //   ref_fill_random -> the loop of bench::fill_random (bench.cpp:295-302) over
 //                      rng::random_normalized<W> (random.hpp:54-67); bench.cpp

@@ -43,13 +43,18 @@ def _csrc_deps():
     return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "mpfk.h")]
 
 
-def build_lib(force=False, verbose_ptxas=False):
+def build_lib(force=False):
     out = os.path.join(PKG, "libmpfk.so")
     if force or _stale(out, _csrc_deps()):
-        flags = list(NVCC_FLAGS)
-        if verbose_ptxas:
-            flags += ["-Xptxas", "-v"]
-        _run([NVCC, *flags, "-shared", "-o", out, os.path.join(CSRC, "capi.cu")])
+        _run([NVCC, *NVCC_FLAGS, "-shared", "-o", out, os.path.join(CSRC, "capi.cu")])
+    return out
+
+
+def build_tune(force=False):
+    """The tile-configuration sweep library (scripts/tune.py); not the product."""
+    out = os.path.join(PKG, "libmpfk_tune.so")
+    if force or _stale(out, _csrc_deps()):
+        _run([NVCC, *NVCC_FLAGS, "-shared", "-o", out, os.path.join(CSRC, "tune.cu")])
     return out
 
 
