@@ -1,7 +1,7 @@
 // ref_driver.cpp -- a C-ABI shim over the UNMODIFIED reference (mpfkit).
 //
 // TEST INFRASTRUCTURE ONLY (the checker and the reported CPU baseline; never
-// the shipped path).  Compiled by oracle/build_ref.sh together with the
+// the shipped path).  Compiled by oracle/Makefile together with the
 // reference's own proj/src/runtime.cpp and proj/src/linalg.cpp, straight from
 // where they lie under /root/reference, into oracle/_ref/libmpfkref.so.  No
 // reference source is copied into this repository.
