@@ -342,36 +342,31 @@ MPFK_HD void merge6(const double* x, const double* y, double* z) {
 
 // VecSumErrBranch with k = 3 slots over n = 6 inputs (eft.hpp:205-225),
 // including its early exit once the last slot is final.
+// Branch-free: the slot writes are selects on (live, j); after the early
+// exit the remaining quick-two-sums still execute but nothing they produce
+// is kept, exactly as if the reference had returned.
 MPFK_HD void vseb_3_6(const double* e, double* out) {
   double o0 = 0.0, o1 = 0.0, o2 = 0.0;
   int j = 0;
-  bool done = false;
+  bool live = true;  // !done
   double eps = e[0];
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
     double s, r;
     qts(eps, e[i + 1], s, r);
-    if (!done) {
-      if (j == 0) o0 = s;
-      else if (j == 1) o1 = s;
-      else o2 = s;
-      if (nz(r)) {
-        if (j >= 2) {
-          done = true;
-        } else {
-          ++j;
-          eps = r;
-        }
-      } else {
-        eps = s;
-      }
-    }
+    o0 = sel(live && j == 0, s, o0);
+    o1 = sel(live && j == 1, s, o1);
+    o2 = sel(live && j == 2, s, o2);
+    const bool nzr = nz(r);
+    const bool adv = live && nzr && j < 2;  // finalise slot j, open j + 1 with r
+    eps = sel(live, sel(nzr, r, s), eps);   // (eps is dead once the slots are full)
+    live = live && !(nzr && j >= 2);        // out of slots: drop the rest
+    j += adv ? 1 : 0;
   }
-  if (!done && nz(eps)) {
-    if (j == 0) o0 = eps;
-    else if (j == 1) o1 = eps;
-    else o2 = eps;
-  }
+  const bool tail = live && nz(eps);
+  o0 = sel(tail && j == 0, eps, o0);
+  o1 = sel(tail && j == 1, eps, o1);
+  o2 = sel(tail && j == 2, eps, o2);
   out[0] = o0, out[1] = o1, out[2] = o2;
 }
 
