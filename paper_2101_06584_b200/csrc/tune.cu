@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "gemm_kernel.cuh"
+#include "gemm_tma.cuh"
 
 using namespace mpfk::kern;
 
@@ -27,6 +28,21 @@ cudaError_t run_cfg(const GemmArgs& g, cudaStream_t s) {
 }
 
 template <class Cfg>
+cudaError_t run_tma_cfg(const GemmArgs& g, cudaStream_t s) {
+  return launch_tma<Cfg>(g, s);
+}
+
+template <class Cfg>
+cudaError_t info_tma_cfg(int* regs, int* smem, int* threads) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, mpgemm_tma_kernel<Cfg>);
+  *regs = a.numRegs;
+  *smem = (int)TmaLayout<Cfg>::SMEM;
+  *threads = Cfg::THREADS;
+  return e;
+}
+
+template <class Cfg>
 cudaError_t info_cfg(int* regs, int* smem, int* threads) {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, mpgemm_kernel<Cfg>);
@@ -40,23 +56,22 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
   {W, #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB,           \
    run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>, info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
 
+#define T(W, BM, BN, BK, TM, TN, ST, KU, GM, MB)                                                   \
+  {W, "tma/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB,     \
+   run_tma_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>,                                    \
+   info_tma_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
+
 const Entry kEntries[] = {
+    T(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),
+    T(2, 64, 64, 16, 4, 4, 3, 2, 16, 2),
+    T(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),
+    T(3, 32, 32, 16, 2, 2, 3, 1, 16, 3),
+    T(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),
+    T(4, 16, 32, 16, 1, 2, 3, 1, 16, 3),
+    T(4, 16, 32, 16, 1, 2, 4, 1, 16, 3),
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),
-    E(2, 64, 64, 16, 4, 4, 2, 4, 16, 2),
-    E(2, 64, 64, 16, 4, 4, 2, 8, 16, 2),
-    E(2, 64, 64, 16, 4, 4, 2, 16, 16, 2),
-    E(2, 64, 64, 16, 4, 4, 3, 4, 16, 2),
-    E(2, 32, 32, 16, 2, 2, 2, 4, 16, 4),
     E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),
-    E(3, 32, 32, 16, 2, 2, 2, 2, 16, 3),
-    E(3, 32, 32, 16, 2, 2, 2, 4, 16, 3),
-    E(3, 16, 32, 16, 1, 2, 2, 2, 16, 4),
     E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),
-    E(4, 16, 32, 16, 1, 2, 2, 2, 16, 3),
-    E(4, 32, 16, 16, 2, 1, 2, 2, 16, 3),
-    E(4, 32, 32, 16, 2, 2, 2, 2, 16, 2),
-    E(4, 16, 16, 16, 1, 1, 2, 2, 16, 4),
-    E(4, 16, 64, 16, 1, 4, 2, 1, 16, 2),
 };
 }  // namespace
 
