@@ -226,6 +226,7 @@ def run_mpfk(args, ws, rank, local):
     W, n, wide = WORKLOADS[args.workload]
     m = k = n
     torch.cuda.set_device(local)
+    P.set_device(local)  # libmpfk has its own CUDA runtime: mirror the choice
     dev = torch.device("cuda", local)
     use_dist = ws > 1 or args.dist
     if use_dist and not dist.is_initialized():

@@ -84,6 +84,13 @@ const char *mpfk_last_error(void);
 int mpfk_abi_version(void);
 /* number of usable devices (0 when none); never fails */
 int mpfk_device_count(void);
+/* Make `dev` the calling thread's current device for libmpfk (and
+ * initialise it).  libmpfk carries its own CUDA runtime; a host framework
+ * that selected a device with its runtime (e.g. torch.cuda.set_device under
+ * torchrun) should mirror that choice here.  mpfk_get_device returns the
+ * current device (-1 when none). */
+int mpfk_set_device(int dev);
+int mpfk_get_device(void);
 /* Device self-test on the current device: binary64 round-to-nearest-even and
  * a correctly rounded fused multiply-add (runtime.cpp:19-38). */
 int mpfk_selftest(void);

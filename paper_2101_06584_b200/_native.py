@@ -57,6 +57,8 @@ _SIGS = {
     "mpfk_init": (C.c_int, [C.c_int]),
     "mpfk_shutdown": (None, []),
     "mpfk_selftest": (C.c_int, []),
+    "mpfk_set_device": (C.c_int, [C.c_int]),
+    "mpfk_get_device": (C.c_int, []),
     "mpfk_matmul_block_parallel_into": (C.c_int, [C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat),
                                                   C.POINTER(MpfkMat), _U64, C.c_int, C.c_uint]),
     "mpfk_matmul_block_into": (C.c_int, [C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat),

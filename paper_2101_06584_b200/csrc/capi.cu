@@ -852,6 +852,25 @@ void mpfk_shutdown(void) {
   cudaSetDevice(prev);
 }
 
+int mpfk_set_device(int dev) {
+  return guarded([&] {
+    const int n = mpfk_device_count();
+    if (n == 0) fail(MPFK_ENODEV, "mpfk: no CUDA sm_100 device is visible; the GPU library has no CPU fallback");
+    if (dev < 0 || dev >= n) fail(MPFK_EINVAL, "mpfk: device index out of range");
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+    ensure_devices(1, dev);
+  });
+}
+
+int mpfk_get_device(void) {
+  int d = -1;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return d;
+}
+
 int mpfk_selftest(void) {
   return guarded([&] {
     if (mpfk_device_count() == 0)

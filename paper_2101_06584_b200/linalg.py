@@ -362,6 +362,15 @@ def fp64_peak() -> tuple:
     return ops.value, ms.value
 
 
+def set_device(dev: int):
+    """Make `dev` libmpfk's current device (mirror torch.cuda.set_device)."""
+    N.check(N.lib().mpfk_set_device(int(dev)))
+
+
+def get_device() -> int:
+    return N.lib().mpfk_get_device()
+
+
 def device_count() -> int:
     return N.lib().mpfk_device_count()
 

@@ -107,3 +107,14 @@ def test_device_api_on_submatrices(gpu_lib):
     sub = np.ascontiguousarray(big[:, r0:r0 + m, c0:c0 + k])
     want = O.ref_gemm(sub, B, k, 17)
     assert mismatches(dC.cpu().numpy(), want) == 0
+
+
+def test_set_device_mirrors_torch(gpu_lib):
+    import torch
+    P = gpu_lib
+    torch.cuda.set_device(0)
+    assert P.get_device() == 0
+    P.set_device(0)
+    assert P.get_device() == 0
+    with pytest.raises(ValueError, match="device index out of range"):
+        P.set_device(P.device_count())
