@@ -434,7 +434,7 @@ uint64_t pad4(uint64_t c) { return (c + 3) & ~uint64_t(3); }
 
 // host pads of C -> +0 (zero_pads, linalg.hpp:99-106)
 void zero_host_pads(int W, mpfk_mat* C) {
-  if (C->stride == C->cols) return;
+  if (C->stride == C->cols || !C->base || C->rows == 0) return;
   const uint64_t pc = plane_of(C);
   for (int w = 0; w < W; ++w)
     for (uint64_t i = 0; i < C->rows; ++i)

@@ -62,10 +62,11 @@ __device__ __forceinline__ void cp_async_wait() {
 // and share their A and B panels in L2 instead of streaming all of B per
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
-          int GROUP_M_ = 16, int MINB_ = 1>
+          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0>
 struct TileCfg {
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
   static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
+  static constexpr int FIXK = FIXK_;  // full k-tiles run a constant-trip loop
   static constexpr int TX = BN / TN;  // threads along N
   static constexpr int TY = BM / TM;  // threads along M
   static constexpr int THREADS = TX * TY;
@@ -119,6 +120,31 @@ __device__ __forceinline__ void tile_coords(int lin, int tiles_m, int tiles_n, i
   const int local = lin - band * GROUP_M * tiles_n;
   tm = first + local % rows;
   tn = local / rows;
+}
+
+// one k step of the register micro-tile: C (+)= A(:, kk) * B(kk, :)
+template <class Cfg>
+__device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W], const double* As,
+                                         const double* Bs, int tx, int ty, int kk) {
+  constexpr int W = Cfg::W, BM = Cfg::BM, BK = Cfg::BK, TM = Cfg::TM, TN = Cfg::TN;
+  constexpr int TX = Cfg::TX, TY = Cfg::TY;
+  double a[TM][W], b[TN][W];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
+#pragma unroll
+  for (int j = 0; j < TN; ++j)
+#pragma unroll
+    for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + kk * Cfg::BS + tx + j * TX];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      double p[W];
+      arith::mp_mul<W>(a[i], b[j], p);
+      arith::mp_add<W>(acc[i][j], p, acc[i][j]);
+    }
 }
 
 template <class Cfg>
@@ -202,25 +228,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         for (int j = 0; j < TN; ++j) arith::mp_mul<W>(a[i], b[j], acc[i][j]);
       kk = 1;
     }
+    if (Cfg::FIXK && kk == 0 && kend == BK) {
 #pragma unroll Cfg::KUNROLL
-    for (; kk < kend; ++kk) {
-      double a[TM][W], b[TN][W];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
-#pragma unroll
-      for (int j = 0; j < TN; ++j)
-#pragma unroll
-        for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + kk * Cfg::BS + tx + j * TX];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) {
-          double p[W];
-          arith::mp_mul<W>(a[i], b[j], p);
-          arith::mp_add<W>(acc[i][j], p, acc[i][j]);
-        }
+      for (int q = 0; q < BK; ++q) mac_step<Cfg>(acc, As, Bs, tx, ty, q);
+    } else {
+#pragma unroll Cfg::KUNROLL
+      for (; kk < kend; ++kk) mac_step<Cfg>(acc, As, Bs, tx, ty, kk);
     }
     __syncthreads();
   }

@@ -61,17 +61,22 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    run_tma_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>,                                    \
    info_tma_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
 
+#define F(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX)                                                \
+  {W, #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB "/fixk" #FX,  \
+   run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>,                                      \
+   info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>}
+
 const Entry kEntries[] = {
-    T(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),
-    T(2, 64, 64, 16, 4, 4, 3, 2, 16, 2),
-    T(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),
-    T(3, 32, 32, 16, 2, 2, 3, 1, 16, 3),
-    T(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),
-    T(4, 16, 32, 16, 1, 2, 3, 1, 16, 3),
-    T(4, 16, 32, 16, 1, 2, 4, 1, 16, 3),
-    E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),
-    E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),
-    E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),
+    F(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 0),
+    F(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 1),
+    F(2, 64, 64, 16, 4, 4, 2, 4, 16, 2, 1),
+    F(2, 64, 64, 16, 4, 4, 2, 1, 16, 2, 1),
+    F(3, 32, 32, 16, 2, 2, 2, 1, 16, 3, 0),
+    F(3, 32, 32, 16, 2, 2, 2, 1, 16, 3, 1),
+    F(3, 32, 32, 16, 2, 2, 2, 2, 16, 3, 1),
+    F(4, 16, 32, 16, 1, 2, 2, 1, 16, 3, 0),
+    F(4, 16, 32, 16, 1, 2, 2, 1, 16, 3, 1),
+    F(4, 16, 32, 16, 1, 2, 2, 2, 16, 3, 1),
 };
 }  // namespace
 
