@@ -180,8 +180,9 @@ int mpfk_ew_device(int width, int op, uint64_t rows, uint64_t cols, double *out,
 
 /* r[i] = op(x[i], y[i]) for `count` values stored AoS (W doubles each) in
  * host memory, computed on the GPU.  op: 0 = add, 1 = mul (library
- * defaults for the width, mpf.hpp:242-260).  Used by the arithmetic parity
- * sweeps. */
+ * defaults for the width, mpf.hpp:242-260); width 3 also 2 = td_mul_q
+ * (mpf.hpp:167-174) and 3 = td_add_merge (:125-131).  Used by the
+ * arithmetic parity sweeps. */
 int mpfk_binop_batch(int width, int op, uint64_t count, const double *x, const double *y,
                      double *r);
 
@@ -206,6 +207,11 @@ int mpfk_mpfm_save_device(const char *path, int width, const double *dev, uint64
  * rows x cols (see mpfk_mpfm_info). */
 int mpfk_mpfm_load_host(const char *path, int width, mpfk_mat *m);
 int mpfk_mpfm_save_host(const char *path, int width, const mpfk_mat *m);
+
+/* The EFT primitives on the GPU over `count` operand pairs (host arrays):
+ * op 0 two_sum, 1 quick_two_sum, 2 two_prod (eft.hpp:46-67).  s + e is the
+ * exact result (acceptance criterion 1). */
+int mpfk_eft_batch(int op, uint64_t count, const double *a, const double *b, double *s, double *e);
 
 /* ---- op counters (linalg.hpp:160-180, linalg.cpp:10-25) ----------------- */
 void mpfk_op_counters_reset(void);

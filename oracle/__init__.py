@@ -86,6 +86,8 @@ def ref():
         L.ref_leaf_multiplies.restype = _U64
         L.ref_ew.argtypes = [C.c_int, C.c_int, C.c_int, _S, _S, _D, _S, _D, _S, _D, _S]
         L.ref_td_add_merge_batch.argtypes = [_S, _D, _D, _D]
+        L.ref_td_mul_q_batch.argtypes = [_S, _D, _D, _D]
+        L.ref_eft_batch.argtypes = [C.c_int, _S, _D, _D, _D, _D]
         _ref = L
     return _ref
 

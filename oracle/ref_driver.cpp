@@ -242,6 +242,27 @@ int ref_ew(int W, int op, int variant, std::size_t rows, std::size_t cols, const
   return 1;
 }
 
+// EFT primitives over a batch: op 0 two_sum, 1 quick_two_sum, 2 two_prod
+void ref_eft_batch(int op, std::size_t count, const double* a, const double* b, double* s,
+                   double* e) {
+  for (std::size_t i = 0; i < count; ++i) {
+    const auto p = op == 0 ? eft::ScalarEft::two_sum(a[i], b[i])
+                           : (op == 1 ? eft::ScalarEft::quick_two_sum(a[i], b[i])
+                                      : eft::ScalarEft::two_prod(a[i], b[i]));
+    s[i] = p.s, e[i] = p.e;
+  }
+}
+
+// td_mul_q over a batch (mpf.hpp:323-327)
+void ref_td_mul_q_batch(std::size_t count, const double* x, const double* y, double* r) {
+  for (std::size_t i = 0; i < count; ++i) {
+    const mpf::Double3 a{{x[3 * i], x[3 * i + 1], x[3 * i + 2]}};
+    const mpf::Double3 b{{y[3 * i], y[3 * i + 1], y[3 * i + 2]}};
+    const auto c = mpf::td_mul_q(a, b);
+    for (int w = 0; w < 3; ++w) r[3 * i + w] = c.c[w];
+  }
+}
+
 // td_add_merge over a batch (mpf.hpp:305-309)
 void ref_td_add_merge_batch(std::size_t count, const double* x, const double* y, double* r) {
   for (std::size_t i = 0; i < count; ++i) {

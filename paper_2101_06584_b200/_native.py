@@ -83,6 +83,7 @@ _SIGS = {
     "mpfk_mpfm_save_host": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(MpfkMat)]),
     "mpfk_gemm_device_acc": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                        _U64, _P, C.POINTER(C.c_int)]),
+    "mpfk_eft_batch": (C.c_int, [C.c_int, _U64, _P, _P, _P, _P]),
     "mpfk_binop_batch": (C.c_int, [C.c_int, C.c_int, _U64, _P, _P, _P]),
     "mpfk_op_counters_reset": (None, []),
     "mpfk_op_counters_read": (None, [C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)]),

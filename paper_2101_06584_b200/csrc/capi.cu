@@ -693,10 +693,27 @@ __global__ void binop_kernel(int op, long long count, const double* x, const dou
     for (int w = 0; w < W; ++w) a[w] = x[i * W + w], b[w] = y[i * W + w];
     if (op == 0)
       arith::mp_add<W>(a, b, c);
-    else
+    else if (op == 1 || W != 3)
       arith::mp_mul<W>(a, b, c);
+    else if (op == 2)
+      arith::td_mul_q(a, b, c);
+    else
+      arith::td_add_merge(a, b, c);
 #pragma unroll
     for (int w = 0; w < W; ++w) r[i * W + w] = c[w];
+  }
+}
+
+// EFT primitives over a batch (acceptance criterion 1): op 0 two_sum,
+// 1 quick_two_sum, 2 two_prod (eft.hpp:46-67)
+__global__ void eft_kernel(int op, long long count, const double* a, const double* b, double* s, double* e) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    double x, y;
+    if (op == 0) arith::two_sum(a[i], b[i], x, y);
+    else if (op == 1) arith::qts(a[i], b[i], x, y);
+    else arith::two_prod(a[i], b[i], x, y);
+    s[i] = x, e[i] = y;
   }
 }
 
@@ -1093,11 +1110,32 @@ int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const do
   });
 }
 
+int mpfk_eft_batch(int op, uint64_t count, const double* a, const double* b, double* s, double* e) {
+  return guarded([&] {
+    if (op < 0 || op > 2) fail(MPFK_EINVAL, "mpfk: eft op must be 0 (two_sum), 1 (quick_two_sum) or 2 (two_prod)");
+    if (count == 0) return;
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    const size_t bytes = sizeof(double) * count;
+    double* d = nullptr;
+    ck(cudaMalloc(&d, 4 * bytes), "cudaMalloc");
+    ck(cudaMemcpy(d, a, bytes, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(d + count, b, bytes, cudaMemcpyHostToDevice), "H2D");
+    const int blocks = (int)std::min<uint64_t>((count + 255) / 256, 148 * 16);
+    eft_kernel<<<blocks, 256>>>(op, (long long)count, d, d + count, d + 2 * count, d + 3 * count);
+    ck(cudaGetLastError(), "eft launch");
+    ck(cudaMemcpy(s, d + 2 * count, bytes, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(e, d + 3 * count, bytes, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d);
+  });
+}
+
 int mpfk_binop_batch(int width, int op, uint64_t count, const double* x, const double* y,
                      double* r) {
   return guarded([&] {
     check_width(width);
-    if (op != 0 && op != 1) fail(MPFK_EINVAL, "mpfk: op must be 0 (add) or 1 (mul)");
+    if (op < 0 || op > 3 || (op >= 2 && width != 3))
+      fail(MPFK_EINVAL, "mpfk: op must be 0 (add), 1 (mul), or for width 3 2 (td_mul_q) / 3 (td_add_merge)");
     if (count == 0) return;
     const int dev = current_device();
     ensure_devices(1, dev);

@@ -386,6 +386,16 @@ MPFK_HD void td_add_merge(const double* x, const double* y, double* r) {
   vseb_3_6(e, r);
 }
 
+// td_mul_q, mpf.hpp:167-174: zero-extend, quad multiply, truncate (not a
+// library default; the comparison kernel of the paper's TD table).
+MPFK_HD void td_mul_q(const double* x, const double* y, double* r) {
+  const double xx[4] = {x[0], x[1], x[2], 0.0};
+  const double yy[4] = {y[0], y[1], y[2], 0.0};
+  double rr[4];
+  qd_mul(xx, yy, rr);
+  r[0] = rr[0], r[1] = rr[1], r[2] = rr[2];
+}
+
 // Library width defaults, mpf.hpp:242-260.
 template <int W>
 MPFK_HD void mp_add(const double* x, const double* y, double* r) {

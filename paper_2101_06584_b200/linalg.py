@@ -339,9 +339,20 @@ def binop_batch(W: int, op: str, x: np.ndarray, y: np.ndarray) -> np.ndarray:
     if x.shape != y.shape or x.ndim != 2 or x.shape[1] != W:
         raise ValueError("binop_batch: x and y must be (count, W)")
     r = np.empty_like(x)
-    N.check(N.lib().mpfk_binop_batch(W, {"add": 0, "mul": 1}[op], x.shape[0], x.ctypes.data, y.ctypes.data,
+    N.check(N.lib().mpfk_binop_batch(W, {"add": 0, "mul": 1, "td_mul_q": 2, "td_add_merge": 3}[op], x.shape[0],
+                                     x.ctypes.data, y.ctypes.data,
                                      r.ctypes.data))
     return r
+
+
+def eft_batch(op: str, a: np.ndarray, b: np.ndarray):
+    """two_sum / quick_two_sum / two_prod of float64 arrays on the GPU -> (s, e)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    s, e = np.empty_like(a), np.empty_like(a)
+    code = {"two_sum": 0, "quick_two_sum": 1, "two_prod": 2}[op]
+    N.check(N.lib().mpfk_eft_batch(code, a.size, a.ctypes.data, b.ctypes.data, s.ctypes.data, e.ctypes.data))
+    return s, e
 
 
 def fill_baseline(W: int, rows: int, cols: int, seed: int, wide: bool = False, pinned: bool = False,
