@@ -240,7 +240,7 @@ def criterion8():
         t0 = time.perf_counter()
         P.matmul_block(A, B)
         tg = time.perf_counter() - t0
-        rows = 64
+        rows = min(n, 32 * (os.cpu_count() or 1))  # one 32-row block per reference thread
         t0 = time.perf_counter()
         O.ref_gemm(np.ascontiguousarray(A.data[:, :rows]), B.data, n, n, workers=os.cpu_count())
         tc = (time.perf_counter() - t0) * n / rows
