@@ -15,8 +15,10 @@ from bench import WORKLOADS  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="dd8192")
 ap.add_argument("--launches", type=int, default=2)
+ap.add_argument("--n", type=int, default=0, help="override the workload's size")
 a = ap.parse_args()
 W, n, wide = WORKLOADS[a.workload]
+n = a.n or n
 ld = P.pad_columns(n)
 A = torch.from_numpy(P.fill_baseline(W, n, n, 1, wide=wide).data).cuda()
 B = torch.from_numpy(P.fill_baseline(W, n, n, 2, wide=wide).data).cuda()
