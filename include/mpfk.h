@@ -158,6 +158,30 @@ int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const do
                          uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, void *stream,
                          int *launches);
 
+/* Fused all-gather -> GEMM in ONE kernel: B is not resident on this device;
+ * its rows [src_row0[s], src_row0[s+1]) live in source slice s (nsrc <= 8),
+ * typically other GPUs' memory mapped over NVLink (mpfk_ipc_open), each a
+ * W-plane (rows_s x ldb) array.  The GEMM kernel pulls B's K panels
+ * (panel_rows rows, a multiple of 16) into the local buffer B on demand, in
+ * chunks of chunk_rows handed out by atomic counters, so the transfer
+ * overlaps the FP64 work tile by tile and every panel crosses the link once
+ * per GPU.  Bit-identical to mpfk_gemm_device; after the call B holds the
+ * whole matrix.  Source slices must stay unchanged until the call completes
+ * on the stream. */
+int mpfk_gemm_device_pull(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                          uint64_t lda, uint64_t a_plane, double *B, uint64_t ldb, uint64_t b_plane,
+                          double *C, uint64_t ldc, uint64_t c_plane, int nsrc,
+                          const double *const *src, const uint64_t *src_row0, uint64_t panel_rows,
+                          uint64_t chunk_rows, void *stream, int *launches);
+/* device memory and CUDA IPC plumbing for the fused path (one process per
+ * GPU): handles are 64-byte cudaIpcMemHandle_t blobs. */
+int mpfk_device_alloc(uint64_t bytes, void **ptr);
+int mpfk_device_free(void *ptr);
+int mpfk_memcpy(void *dst, const void *src, uint64_t bytes);
+int mpfk_ipc_get_handle(const void *dev_ptr, void *handle_out);
+int mpfk_ipc_open(const void *handle, void **dev_ptr);
+int mpfk_ipc_close(void *dev_ptr);
+
 /* ---- elementwise width kernels (mpf::add/mul<W>, mpf.hpp:341-353) ------- */
 
 /* EwOp, linalg.hpp:623 */

@@ -83,6 +83,15 @@ _SIGS = {
     "mpfk_mpfm_save_host": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(MpfkMat)]),
     "mpfk_gemm_device_acc": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                        _U64, _P, C.POINTER(C.c_int)]),
+    "mpfk_gemm_device_pull": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
+                                        _U64, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_U64), _U64, _U64, _P,
+                                        C.POINTER(C.c_int)]),
+    "mpfk_device_alloc": (C.c_int, [_U64, C.POINTER(C.c_void_p)]),
+    "mpfk_device_free": (C.c_int, [_P]),
+    "mpfk_memcpy": (C.c_int, [_P, _P, _U64]),
+    "mpfk_ipc_get_handle": (C.c_int, [_P, _P]),
+    "mpfk_ipc_open": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "mpfk_ipc_close": (C.c_int, [_P]),
     "mpfk_eft_batch": (C.c_int, [C.c_int, _U64, _P, _P, _P, _P]),
     "mpfk_binop_batch": (C.c_int, [C.c_int, C.c_int, _U64, _P, _P, _P]),
     "mpfk_op_counters_reset": (None, []),

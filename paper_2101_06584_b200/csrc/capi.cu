@@ -346,6 +346,39 @@ int enqueue_gemm_batched(int W, int batch, uint64_t m, uint64_t n, uint64_t k, c
   return dispatch_gemm(W, g, s);
 }
 
+template <class Cfg>
+void launch_pull_cfg(const kern::GemmArgs& g, const kern::PullB& P, cudaStream_t s) {
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    ck(cudaFuncSetAttribute(kern::mpgemm_pull_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)Cfg::SMEM),
+       "cudaFuncSetAttribute");
+    configured_dev = dev;
+  }
+  if (P.panel_rows % Cfg::BK) fail(MPFK_EINVAL, "mpfk: panel_rows must be a multiple of 16");
+  const long long tiles = tiles_of<Cfg>(g);
+  if (tiles > 0x7fffffffLL) fail(MPFK_EINVAL, "mpfk: too many tiles");
+  kern::mpgemm_pull_kernel<Cfg><<<(unsigned)tiles, Cfg::THREADS, Cfg::SMEM, s>>>(g, P);
+  ck(cudaGetLastError(), "fused all-gather GEMM launch");
+}
+
+int dispatch_gemm_pull(int W, const kern::GemmArgs& g, const kern::PullB& P, cudaStream_t s) {
+  switch (W) {
+    case 2:
+      if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
+        launch_pull_cfg<Cfg2s>(g, P, s);
+      else
+        launch_pull_cfg<Cfg2>(g, P, s);
+      break;
+    case 3: launch_pull_cfg<Cfg3>(g, P, s); break;
+    case 4: launch_pull_cfg<Cfg4>(g, P, s); break;
+    default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
+  }
+  return 1;
+}
+
 int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s) {
   switch (W) {
     case 2:
@@ -1107,6 +1140,113 @@ int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const do
       g_adds.fetch_add(m * n * k, std::memory_order_relaxed);
     }
     if (launches) *launches = l;
+  });
+}
+
+int mpfk_gemm_device_pull(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                          uint64_t a_plane, double* B, uint64_t ldb, uint64_t b_plane, double* C, uint64_t ldc,
+                          uint64_t c_plane, int nsrc, const double* const* src, const uint64_t* src_row0,
+                          uint64_t panel_rows, uint64_t chunk_rows, void* stream, int* launches) {
+  return guarded([&] {
+    check_width(width);
+    if (nsrc < 1 || nsrc > 8) fail(MPFK_EINVAL, "mpfk: 1..8 source slices");
+    if (!src || !src_row0) fail(MPFK_EINVAL, "mpfk: null source table");
+    if (src_row0[0] != 0 || src_row0[nsrc] != k) fail(MPFK_EINVAL, "mpfk: source slices must cover rows [0, k)");
+    for (int s_ = 0; s_ < nsrc; ++s_)
+      if (src_row0[s_ + 1] < src_row0[s_]) fail(MPFK_EINVAL, "mpfk: source slices out of order");
+    if (panel_rows < 16 || panel_rows % 16 || chunk_rows < 1)
+      fail(MPFK_EINVAL, "mpfk: panel_rows must be a positive multiple of 16 and chunk_rows >= 1");
+    if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
+    if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
+      fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+      fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+    for (int s_ = 0; s_ < nsrc; ++s_)
+      if (reinterpret_cast<uintptr_t>(src[s_]) & 15) fail(MPFK_EINVAL, "mpfk: source slices must be 16-byte aligned");
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int l = 0;
+    if (m && n && k) {
+      if (m > 0x7fffffffULL || n > 0x7fffffffULL || k > 0x7fffffffULL)
+        fail(MPFK_EINVAL, "mpfk: dimension exceeds 2^31-1");
+      kern::PullB P{};
+      P.panel_rows = (int)panel_rows;
+      P.panels = (int)((k + panel_rows - 1) / panel_rows);
+      P.chunk_rows = (int)std::min<uint64_t>(chunk_rows, panel_rows);
+      P.chunks = (int)((panel_rows + P.chunk_rows - 1) / P.chunk_rows);
+      P.nsrc = nsrc;
+      for (int s_ = 0; s_ <= nsrc; ++s_) P.src_row0[s_] = (int)src_row0[s_];
+      for (int s_ = 0; s_ < nsrc; ++s_) {
+        P.src[s_] = src[s_];
+        P.src_plane[s_] = (long long)((src_row0[s_ + 1] - src_row0[s_]) * ldb);
+      }
+      // the last panel may be short: its tail chunks copy nothing but still count
+      int* ctr = nullptr;
+      ck(cudaMallocAsync(reinterpret_cast<void**>(&ctr), sizeof(int) * 2 * P.panels, s), "cudaMallocAsync");
+      ck(cudaMemsetAsync(ctr, 0, sizeof(int) * 2 * P.panels, s), "cudaMemsetAsync");
+      P.next = ctr, P.done = ctr + P.panels;
+      kern::GemmArgs g;
+      g.A = A, g.B = B, g.C = C;
+      g.lda = (long long)lda, g.ldb = (long long)ldb, g.ldc = (long long)ldc;
+      g.pa = (long long)a_plane, g.pb = (long long)b_plane, g.pc = (long long)c_plane;
+      g.M = (int)m, g.N = (int)n, g.K = (int)k;
+      g.accumulate = 0;
+      g.batch = 1, g.sa = g.sb = g.sc = 0;
+      l = dispatch_gemm_pull(width, g, P, s);
+      ck(cudaFreeAsync(ctr, s), "cudaFreeAsync");
+    } else {
+      l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, s);
+    }
+    count_matmul(m, n, k);
+    if (launches) *launches = l;
+  });
+}
+
+int mpfk_device_alloc(uint64_t bytes, void** ptr) {
+  return guarded([&] {
+    if (!ptr) fail(MPFK_EINVAL, "mpfk: null output pointer");
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    *ptr = nullptr;
+    ck(cudaMalloc(ptr, std::max<uint64_t>(bytes, 1)), "cudaMalloc");
+  });
+}
+
+int mpfk_device_free(void* ptr) {
+  return guarded([&] {
+    if (ptr) ck(cudaFree(ptr), "cudaFree");
+  });
+}
+
+int mpfk_memcpy(void* dst, const void* src, uint64_t bytes) {
+  return guarded([&] {
+    if (bytes) ck(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault), "cudaMemcpy");
+  });
+}
+
+int mpfk_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  return guarded([&] {
+    if (!handle_out) fail(MPFK_EINVAL, "mpfk: null handle buffer");
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)), "cudaIpcGetMemHandle");
+    std::memcpy(handle_out, &h, sizeof h);
+  });
+}
+
+int mpfk_ipc_open(const void* handle, void** dev_ptr) {
+  return guarded([&] {
+    if (!handle || !dev_ptr) fail(MPFK_EINVAL, "mpfk: null handle or output pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    *dev_ptr = nullptr;
+    ck(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+
+int mpfk_ipc_close(void* dev_ptr) {
+  return guarded([&] {
+    if (dev_ptr) ck(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
   });
 }
 

@@ -46,6 +46,28 @@ struct GemmArgs {
   long long sa, sb, sc;
 };
 
+// Fused all-gather -> GEMM (mpgemm_kernel<Cfg, true>): B is not resident
+// yet; its rows live in up to 8 source slices (other ranks' memory reached
+// over NVLink peer mappings, or local buffers when emulated on one GPU).
+// Before a CTA stages the k-tile of panel p it makes sure panel p has been
+// copied into the local B: chunks of the panel are handed out by an atomic
+// counter, the CTA copies every chunk it wins (16-byte loads from the
+// owning slice, stores into local B), publishes each with a release fence +
+// done-counter, then waits for the panel's other chunks -- which are being
+// copied by CTAs that are running (they took them), so nothing waits on a
+// CTA that is not resident.  Each panel crosses NVLink once per GPU, while
+// the rest of the grid computes on the panels already present.
+struct PullB {
+  int panels, panel_rows;  // K rows per panel (a multiple of BK)
+  int chunk_rows, chunks;  // chunks per panel
+  int nsrc;                // source slices
+  int src_row0[9];         // slice s holds B rows [src_row0[s], src_row0[s+1])
+  const double* src[8];    // slice s: W planes of (rows_s x ldb), plane stride src_plane[s]
+  long long src_plane[8];
+  int* next;               // [panels] chunk tickets handed out
+  int* done;               // [panels] chunks copied and published
+};
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const int n = valid ? 16 : 0;  // src-size 0 -> 16 zero bytes, no global read
@@ -122,6 +144,64 @@ __device__ __forceinline__ void tile_coords(int lin, int tiles_m, int tiles_n, i
   tn = local / rows;
 }
 
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Copy chunk c of panel p from its source slices into the local B.
+template <int W>
+__device__ __forceinline__ void pull_chunk(const PullB& P, const GemmArgs& g, int p, int c) {
+  const int r0 = p * P.panel_rows + c * P.chunk_rows;
+  const int r1 = min(min(r0 + P.chunk_rows, (p + 1) * P.panel_rows), g.K);
+  if (r1 <= r0) return;
+  const int vpr = (int)(g.ldb / 2);  // 16-byte vectors per row (ld is even)
+  const long long per_plane = (long long)(r1 - r0) * vpr, total = per_plane * W;
+  double* B = const_cast<double*>(g.B);
+  for (long long t = threadIdx.x; t < total; t += blockDim.x) {
+    const int w = (int)(t / per_plane);
+    const long long rem = t - w * per_plane;
+    const int row = r0 + (int)(rem / vpr), v = (int)(rem % vpr);
+    int s = 0;
+    while (s + 1 < P.nsrc && row >= P.src_row0[s + 1]) ++s;
+    const double2* src = reinterpret_cast<const double2*>(P.src[s] + w * P.src_plane[s] +
+                                                          (long long)(row - P.src_row0[s]) * g.ldb) + v;
+    double2* dst = reinterpret_cast<double2*>(B + w * g.pb + (long long)row * g.ldb) + v;
+    *dst = *src;
+  }
+}
+
+// Make panel p of B resident (block-wide; see PullB).
+template <int W>
+__device__ void ensure_panel(const PullB& P, const GemmArgs& g, int p) {
+  __shared__ int s_state;
+  if (threadIdx.x == 0) s_state = ld_acquire_gpu(&P.done[p]) >= P.chunks;
+  __syncthreads();
+  if (s_state) return;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_state = atomicAdd(&P.next[p], 1);
+    __syncthreads();
+    const int c = s_state;
+    if (c >= P.chunks) break;
+    pull_chunk<W>(P, g, p, c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();  // release: the chunk's stores before the count
+      atomicAdd(&P.done[p], 1);
+    }
+  }
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    while (ld_acquire_gpu(&P.done[p]) < P.chunks) {
+      __nanosleep(200);
+      if (clock64() - t0 > (1ll << 36)) __trap();  // ~30 s: a lost chunk, fail loudly
+    }
+  }
+  __syncthreads();
+}
+
 // one k step of the register micro-tile: C (+)= A(:, kk) * B(kk, :)
 template <class Cfg>
 __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W], const double* As,
@@ -147,9 +227,8 @@ __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W]
     }
 }
 
-template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
-    mpgemm_kernel(const GemmArgs g0) {
+template <class Cfg, bool kPull>
+__device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P) {
   constexpr int W = Cfg::W, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, TX = Cfg::TX, TY = Cfg::TY;
   constexpr int STAGES = Cfg::STAGES;
@@ -189,7 +268,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   // prologue: fill STAGES-1 stages
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_tile<Cfg>(As0 + s * Cfg::A_STAGE, Bs0 + s * Cfg::B_STAGE, g, m0, n0, s * BK);
+    if (s < ktiles) {
+      if (kPull) ensure_panel<W>(P, g, s * BK / P.panel_rows);
+      load_tile<Cfg>(As0 + s * Cfg::A_STAGE, Bs0 + s * Cfg::B_STAGE, g, m0, n0, s * BK);
+    }
     cp_async_commit();
   }
 
@@ -199,6 +281,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       const int nt = kt + STAGES - 1;
       if (nt < ktiles) {
         const int slot = nt % STAGES;
+        if (kPull) ensure_panel<W>(P, g, nt * BK / P.panel_rows);
         load_tile<Cfg>(As0 + slot * Cfg::A_STAGE, Bs0 + slot * Cfg::B_STAGE, g, m0, n0, nt * BK);
       }
       cp_async_commit();
@@ -252,6 +335,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       for (int w = 0; w < W; ++w) g.C[w * g.pc + (long long)gm * g.ldc + gn] = acc[i][j][w];
     }
   }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_kernel(const GemmArgs g0) {
+  gemm_body<Cfg, false>(g0, PullB{});
+}
+
+// The fused all-gather -> GEMM (see PullB); batch must be 1.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_pull_kernel(const GemmArgs g0, const PullB pull) {
+  gemm_body<Cfg, true>(g0, pull);
 }
 
 }  // namespace kern

@@ -432,3 +432,51 @@ def strassen_device(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plan
     N.check(N.lib().mpfk_strassen_device(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc, c_plane,
                                          cutoff, stream or None, C.byref(launches)))
     return launches.value
+
+
+def gemm_device_pull(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int, ldb: int,
+                     b_plane: int, C_ptr: int, ldc: int, c_plane: int, src_ptrs, src_row0, panel_rows: int = 64,
+                     chunk_rows: int = 8, stream: int = 0) -> int:
+    """Fused all-gather -> GEMM (mpfk_gemm_device_pull): B's rows come from the
+    source slices (peer-mapped device pointers); B_ptr receives the whole B."""
+    ns = len(src_ptrs)
+    srcs = (C.c_void_p * ns)(*src_ptrs)
+    rows = (C.c_uint64 * (ns + 1))(*src_row0)
+    launches = C.c_int(0)
+    N.check(N.lib().mpfk_gemm_device_pull(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc, c_plane,
+                                          ns, srcs, rows, panel_rows, chunk_rows, stream or None,
+                                          C.byref(launches)))
+    return launches.value
+
+
+def ipc_handle(dev_ptr: int) -> bytes:
+    """The 64-byte CUDA IPC handle of a libmpfk device allocation."""
+    buf = (C.c_char * 64)()
+    N.check(N.lib().mpfk_ipc_get_handle(dev_ptr, buf))
+    return bytes(buf)
+
+
+def ipc_open(handle: bytes) -> int:
+    p = C.c_void_p()
+    buf = (C.c_char * 64).from_buffer_copy(handle)
+    N.check(N.lib().mpfk_ipc_open(buf, C.byref(p)))
+    return p.value
+
+
+def ipc_close(dev_ptr: int):
+    N.check(N.lib().mpfk_ipc_close(dev_ptr))
+
+
+def device_alloc(nbytes: int) -> int:
+    p = C.c_void_p()
+    N.check(N.lib().mpfk_device_alloc(nbytes, C.byref(p)))
+    return p.value
+
+
+def device_free(dev_ptr: int):
+    N.check(N.lib().mpfk_device_free(dev_ptr))
+
+
+def memcpy(dst: int, src: int, nbytes: int):
+    """cudaMemcpy with cudaMemcpyDefault (host or device pointers)."""
+    N.check(N.lib().mpfk_memcpy(dst, src, nbytes))
