@@ -63,6 +63,11 @@ def parse():
     ap.add_argument("--panels", type=int, default=4, help="N > 1: K panels for the overlapped broadcast")
     ap.add_argument("--dist", action="store_true",
                     help="initialise the NCCL process group and run the collective path even at N == 1")
+    ap.add_argument("--fused-allgather", action="store_true",
+                    help="B row-sliced across ranks and pulled over NVLink inside the GEMM kernel "
+                         "(mpfk_gemm_device_pull) instead of an NCCL broadcast")
+    ap.add_argument("--pull-panel", type=int, default=256, help="fused all-gather: K rows per panel")
+    ap.add_argument("--pull-chunk", type=int, default=16, help="fused all-gather: rows per copy chunk")
     ap.add_argument("--check", action="store_true",
                     help="after timing, check the sharded step's C bitwise against a plain one-shot GEMM")
     return ap.parse_args()
@@ -251,9 +256,22 @@ def run_mpfk(args, ws, rank, local):
     launches = [0]
 
     overlap = use_dist and not args.no_overlap
+    slices = None
+    if args.fused_allgather:
+        from paper_2101_06584_b200.dist import PeerBSlices
+        slices = PeerBSlices(W, k, ld)
+        c0, c1 = slices.cuts[slices.rank], slices.cuts[slices.rank + 1]
+        slices.upload(P.fill_baseline(W, c1 - c0, n, 2, wide=wide, row0=c0).data)
+        if use_dist:
+            dist.barrier()
 
     def step():
         ev_mid = torch.cuda.Event(enable_timing=True)
+        if slices is not None:
+            # one kernel: pull B's panels from the ranks' slices while computing
+            ev_mid.record(stream)
+            launches[0] += slices.step(W, dA, dB, dC, rows, n, k, args.pull_panel, args.pull_chunk, stream)
+            return ev_mid
         if overlap:
             # B broadcast in K panels, each panel's GEMM gated on its own panel
             ev_mid.record(stream)
@@ -367,6 +385,13 @@ def run_mpfk(args, ws, rank, local):
         # dominant kernel (the GEMM) of rank 0's shard: algorithmic FP64 ops / launch time
         achieved = rows * n * k * ops / (t_kern * 1e-3) / 1e9  # Gop/s
         traffic = load_traffic(args.workload)
+        parallelism = f"row-shard x{ws}"
+        if slices is not None:
+            parallelism += " + fused all-gather->GEMM (B pulled over peer memory inside the GEMM kernel)"
+        elif overlap:
+            parallelism += f" + NCCL broadcast of B in {args.panels} K panels overlapped with the GEMM"
+        elif use_dist:
+            parallelism += " + NCCL broadcast of B"
         line = {
             "metric": METRIC,
             "value": round(value, 3),
@@ -382,10 +407,7 @@ def run_mpfk(args, ws, rank, local):
             "data": "synthetic (BASELINE.json seeded distributions, SplitMix64), generated on the host",
             "config": {"workload": args.workload, "precision": NAMES[W], "m": m, "n": n, "k": k,
                        "inputs": "wide 2^[-30,30]" if wide else "U[-1,1)", "rows_per_rank": rows,
-                       "parallelism": f"row-shard x{ws}" + ((" + NCCL broadcast of B in "
-                                                             f"{args.panels} K panels overlapped with the GEMM"
-                                                             if overlap else " + NCCL broadcast of B")
-                                                            if use_dist else ""),
+                       "parallelism": parallelism,
                        "l2": "flushed between timed steps" if flush is not None else
                              "inputs larger than L2 (126 MB)",
                        "bit_exact": True},
@@ -406,6 +428,10 @@ def run_mpfk(args, ws, rank, local):
         if check is not None:
             line["check_sharded_equals_one_shot"] = check
         emit(line, args)
+    if use_dist:
+        dist.barrier()
+    if slices is not None:
+        slices.close()
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -102,6 +102,69 @@ def sharded_gemm_step_overlapped(W: int, dA, dB, dC, rows: int, n: int, k: int, 
     return launches
 
 
+class PeerBSlices:
+    """B row-sliced across the ranks for the fused all-gather -> GEMM: rank r
+    owns rows [cuts[r], cuts[r+1]) in a libmpfk device allocation exported
+    with CUDA IPC; every rank maps every other rank's slice (NVLink peer
+    memory), so one kernel per rank can pull the panels it needs while it
+    computes (mpfk_gemm_device_pull).  The slices are the SURVEY's "each GPU
+    uploads 1/G of B" layout (8(e)); nothing is broadcast."""
+
+    def __init__(self, W: int, k: int, ld: int, group=None, align: int = 16):
+        import torch.distributed as dist
+        from . import linalg as L
+        self.W, self.k, self.ld = W, k, ld
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.cuts = [shard_rows(k, world, r, align)[0] for r in range(world)] + [k]
+        self.rank, self.world = rank, world
+        self.rows = self.cuts[rank + 1] - self.cuts[rank]
+        self.local = L.device_alloc(max(8 * W * self.rows * ld, 16))
+        self._opened = []
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, L.ipc_handle(self.local), group=group)
+            self.ptrs = []
+            for r in range(world):
+                if r == rank:
+                    self.ptrs.append(self.local)
+                else:
+                    p = L.ipc_open(handles[r])
+                    self._opened.append(p)
+                    self.ptrs.append(p)
+        else:
+            self.ptrs = [self.local]
+
+    def upload(self, host_planes):
+        """host_planes: (W, rows, ld) float64 array of this rank's slice."""
+        from . import linalg as L
+        import numpy as np
+        a = np.ascontiguousarray(host_planes, dtype=np.float64)
+        assert a.shape == (self.W, self.rows, self.ld)
+        if a.size:
+            L.memcpy(self.local, a.ctypes.data, a.nbytes)
+
+    def step(self, W, dA, dB, dC, rows, n, k, panel_rows=256, chunk_rows=16, stream=None) -> int:
+        """C_shard = A_shard * B with B pulled from the slices inside the GEMM."""
+        from . import linalg as L
+        if rows == 0:
+            return 0
+        s = stream.cuda_stream if stream is not None else 0
+        lda, ldb, ldc = dA.shape[2], dB.shape[2], dC.shape[2]
+        return L.gemm_device_pull(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
+                                  dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, self.ptrs, self.cuts,
+                                  panel_rows, chunk_rows, s)
+
+    def close(self):
+        from . import linalg as L
+        for p in self._opened:
+            L.ipc_close(p)
+        self._opened = []
+        if self.local:
+            L.device_free(self.local)
+            self.local = 0
+
+
 def gather_c(dC_shard, m: int, world: int, group=None, align: int = 64):
     """Assemble the replicated (W, m, ld) C from the row shards
     (all-gather); shards are padded to the common span length.  `align`
