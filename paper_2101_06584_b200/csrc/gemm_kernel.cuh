@@ -172,6 +172,28 @@ __device__ __forceinline__ void pull_chunk(const PullB& P, const GemmArgs& g, in
   }
 }
 
+// Copy (without waiting) any still-unclaimed chunks of panel p: the
+// lookahead that lets CTAs entering panel p-1 stage panel p in advance.
+template <int W>
+__device__ void help_panel(const PullB& P, const GemmArgs& g, int p) {
+  __shared__ int s_ticket;
+  if (p >= P.panels) return;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+      s_ticket = ld_acquire_gpu(&P.next[p]) >= P.chunks ? P.chunks : atomicAdd(&P.next[p], 1);
+    __syncthreads();
+    const int c = s_ticket;
+    if (c >= P.chunks) break;
+    pull_chunk<W>(P, g, p, c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&P.done[p], 1);
+    }
+  }
+}
+
 // Make panel p of B resident (block-wide; see PullB).
 template <int W>
 __device__ void ensure_panel(const PullB& P, const GemmArgs& g, int p) {
@@ -265,11 +287,17 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P) {
       }
   }
 
+  int ready_panel = -1;  // kPull: panels [0, ready_panel] are resident (visited in order)
+
   // prologue: fill STAGES-1 stages
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ktiles) {
-      if (kPull) ensure_panel<W>(P, g, s * BK / P.panel_rows);
+      if (kPull && s * BK / P.panel_rows > ready_panel) {
+        ready_panel = s * BK / P.panel_rows;
+        ensure_panel<W>(P, g, ready_panel);
+        help_panel<W>(P, g, ready_panel + 1);
+      }
       load_tile<Cfg>(As0 + s * Cfg::A_STAGE, Bs0 + s * Cfg::B_STAGE, g, m0, n0, s * BK);
     }
     cp_async_commit();
@@ -281,7 +309,11 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P) {
       const int nt = kt + STAGES - 1;
       if (nt < ktiles) {
         const int slot = nt % STAGES;
-        if (kPull) ensure_panel<W>(P, g, nt * BK / P.panel_rows);
+        if (kPull && nt * BK / P.panel_rows > ready_panel) {  // a new panel: once per panel
+          ready_panel = nt * BK / P.panel_rows;
+          ensure_panel<W>(P, g, ready_panel);
+          help_panel<W>(P, g, ready_panel + 1);
+        }
         load_tile<Cfg>(As0 + slot * Cfg::A_STAGE, Bs0 + slot * Cfg::B_STAGE, g, m0, n0, nt * BK);
       }
       cp_async_commit();
