@@ -165,23 +165,18 @@ def matmul_block_parallel_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix, n_min: in
                                variant: KernelVariant = KernelVariant.NORMAL, workers: int = 1):
     """linalg.hpp:402-433 on min(workers, GPUs) devices."""
     W = _check_same_width(C_, A, B)
-    if workers < 1:
-        raise ValueError("matmul: workers must be at least 1")
-    if n_min < 0:
-        raise ValueError("matmul: n_min must be at least 1")
     c, a, b = C_._c(), A._c(), B._c()
-    N.check(N.lib().mpfk_matmul_block_parallel_into(W, C.byref(c), C.byref(a), C.byref(b), int(n_min),
-                                                    int(variant), int(workers)))
+    # negative counts reach the C ABI as 0, which it rejects in the reference's order
+    N.check(N.lib().mpfk_matmul_block_parallel_into(W, C.byref(c), C.byref(a), C.byref(b), max(int(n_min), 0),
+                                                    int(variant), max(int(workers), 0)))
 
 
 def matmul_block_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix, n_min: int = 32,
                       variant: KernelVariant = KernelVariant.NORMAL):
     """linalg.hpp:368-388."""
     W = _check_same_width(C_, A, B)
-    if n_min < 0:
-        raise ValueError("matmul: n_min must be at least 1")
     c, a, b = C_._c(), A._c(), B._c()
-    N.check(N.lib().mpfk_matmul_block_into(W, C.byref(c), C.byref(a), C.byref(b), int(n_min), int(variant)))
+    N.check(N.lib().mpfk_matmul_block_into(W, C.byref(c), C.byref(a), C.byref(b), max(int(n_min), 0), int(variant)))
 
 
 def matmul_naive_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix,
@@ -415,13 +410,10 @@ def matmul_strassen_parallel(A: MPMatrix, B: MPMatrix, cutoff: int = 64, n_min: 
     """linalg::matmul_strassen_parallel (linalg.hpp:596-617); bit-identical to
     the serial form, as in the reference."""
     W = _check_same_width(A, B)
-    if cutoff < 0 or n_min < 0 or workers < 0:
-        raise ValueError("matmul: cutoff must be at least 1" if cutoff < 0 else
-                         "matmul: n_min must be at least 1" if n_min < 0 else "matmul: workers must be at least 1")
     C_ = MPMatrix(W, A.rows(), B.cols())
     c, a, b = C_._c(), A._c(), B._c()
-    N.check(N.lib().mpfk_matmul_strassen(W, C.byref(c), C.byref(a), C.byref(b), int(cutoff), int(n_min),
-                                         int(variant), int(workers)))
+    N.check(N.lib().mpfk_matmul_strassen(W, C.byref(c), C.byref(a), C.byref(b), max(int(cutoff), 0),
+                                         max(int(n_min), 0), int(variant), max(int(workers), 0)))
     return C_
 
 
