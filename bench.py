@@ -342,25 +342,40 @@ def run_mpfk(args, ws, rank, local):
         Ah = P.fill_baseline(W, rows, k, 1, wide=wide, row0=r0, pinned=True)
         Bh2 = P.fill_baseline(W, k, n, 2, wide=wide, pinned=True)
         Ch = P.MPMatrix(W, rows, n, pinned=True)
-        P.matmul_block_parallel_into(Ch, Ah, Bh2, 32, P.KernelVariant.SIMD_LOADSTORE, 1)  # warm
+        if use_dist:
+            # one rank per GPU: each rank copies its A shard and 1/ws of B
+            # from the host; B's panels are all-gathered over NVLink
+            from paper_2101_06584_b200.dist import matmul_sharded_into
+
+            def e2e_call():
+                matmul_sharded_into(Ch, Ah, Bh2, panels=args.panels, device=dev)
+        else:
+            def e2e_call():
+                P.matmul_block_parallel_into(Ch, Ah, Bh2, 32, P.KernelVariant.SIMD_LOADSTORE, 1)
+        e2e_call()  # warm
         e2e_steps = max(1, min(args.steps, 3))
         if use_dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            P.matmul_block_parallel_into(Ch, Ah, Bh2, 32, P.KernelVariant.SIMD_LOADSTORE, 1)
+            e2e_call()
             _ = float(Ch.data[0, 0, 0]) if rows else 0.0  # result read on the host
+        if use_dist:
+            dist.barrier()
         t_e2e = (time.perf_counter() - t0) / e2e_steps
-        st = P.last_stats()
+        st = None if use_dist else P.last_stats()
         if use_dist:
             t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_e2e = t.item()
-        h2d = 8 * W * (m * k + ws * k * n)
+        h2d = 8 * W * (m * k + k * n)  # (ws > 1: each rank copies 1/ws of B)
         d2h = 8 * W * m * n
         e2e = {"value": round(flops / t_e2e / 1e9, 3), "unit": "Gflop/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-               "ms_breakdown_rank0": {k_: round(st[k_], 3) for k_ in ("h2d_ms", "kernel_ms", "d2h_ms", "total_ms")}}
+               "api": "dist.matmul_sharded_into (per rank)" if use_dist else
+                      "matmul_block_parallel_into (C ABI, host buffers)"}
+        if st is not None:
+            e2e["ms_breakdown"] = {k_: round(st[k_], 3) for k_ in ("h2d_ms", "kernel_ms", "d2h_ms", "total_ms")}
         # spot-check the e2e result against the device-resident run (same inputs)
         if rows:
             same = bool((torch.from_numpy(np.ascontiguousarray(Ch.data)).view(torch.int64) ==

@@ -102,6 +102,153 @@ def sharded_gemm_step_overlapped(W: int, dA, dB, dC, rows: int, n: int, k: int, 
     return launches
 
 
+def gather_panels(k: int, panels: int, world: int, align: int = 16):
+    """K panel plan for B starting on the host: panel height pk is a multiple
+    of align*world so every panel splits into `world` equal sub-slices of
+    pk/world rows, rank r uploading sub-slice r.  Returns (pk, [(k0, k1)]);
+    the last panel may be short (k1 - k0 < pk), its missing rows zero."""
+    if k <= 0:
+        return align * world, []
+    panels = max(1, panels)
+    unit = align * world
+    pk = max(unit, ((k + panels - 1) // panels + unit - 1) // unit * unit)
+    return pk, [(k0, min(k, k0 + pk)) for k0 in range(0, k, pk)]
+
+
+def matmul_sharded_into(C_, A, B, *, panels: int = 8, group=None, device=None,
+                        gemm: Optional[Callable] = None) -> int:
+    """This rank's row shard of C = A*B with every operand starting and
+    ending in host memory: the multi-process counterpart of
+    matmul_block_parallel_into (linalg.hpp:402-433), one rank per GPU.
+
+    A, C_: this rank's row shard (host MPMatrix, pinned for overlap); B: the
+    whole K x n right operand, readable by every rank (e.g. an MPFM file
+    mapped on each).  Each rank copies only 1/world of B over its own PCIe
+    link -- sub-slice r of each K panel ("each GPU H2D-copies
+    B's 1/G slice, then all-gather") -- and the panels are assembled on every
+    GPU with NCCL all-gathers queued ahead of the compute.  The GEMM runs
+    panel by panel (mpfk_gemm_device, then mpfk_gemm_device_acc continuing
+    the chains kept in C, linalg.hpp:261), each launch waiting only for its
+    own panel, so the host copies and NVLink traffic overlap the FP64 work.
+    The shard of C is bit-identical to the single-GPU product for any world
+    size.  Collective: every rank of `group` must call it (a rank with no
+    rows passes 0-row A and C).  Returns the number of GEMM launches.
+
+    `gemm(W, A_panel, B_panel, dC, rows, n, kp, ld, accumulate)` overrides
+    the device kernel (the CPU tests pass the oracle)."""
+    import torch
+    import torch.distributed as dist
+    from . import linalg as L
+    L._check_same_width(C_, A, B)
+    if A.cols() != B.rows():
+        raise ValueError("matmul: inner dimensions differ")
+    if C_.rows() != A.rows() or C_.cols() != B.cols():
+        raise ValueError("matmul: result shape mismatch")
+    W, rows, k, n = A.W, A.rows(), A.cols(), B.cols()
+    multi = dist.is_initialized()
+    world = dist.get_world_size(group) if multi else 1
+    rank = dist.get_rank(group) if multi else 0
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else \
+            torch.device("cpu")
+    cuda = device.type == "cuda"
+    if gemm is None and not cuda:
+        raise RuntimeError("matmul_sharded_into: the GEMM runs on a CUDA device (there is no CPU path)")
+    ld = B.stride()
+    pk, parts = gather_panels(k, panels, world)
+    chunk = pk // world
+    f64 = torch.float64
+    dB = torch.empty((W, max(1, len(parts)) * pk, ld), dtype=f64, device=device)
+    piece = torch.zeros((max(1, len(parts)), W, chunk, ld), dtype=f64, device=device)
+    ldc = C_.stride()
+    dC = torch.zeros((W, max(rows, 1), ldc), dtype=f64, device=device)
+    dA = torch.empty((W, max(rows, 1), A.stride()), dtype=f64, device=device)
+    hA, hB, hC = torch.from_numpy(A.data), torch.from_numpy(B.data), torch.from_numpy(C_.data)
+    comp = torch.cuda.current_stream(device) if cuda else None
+    up = torch.cuda.Stream(device) if cuda else None
+    down = torch.cuda.Stream(device) if cuda else None
+
+    def mark(stream):
+        if not cuda:
+            return None
+        e = torch.cuda.Event()
+        e.record(stream)
+        return e
+
+    # host -> device on the copy stream, in the order the GEMMs consume it:
+    # A's shard, then this rank's sub-slice of each K panel (one contiguous
+    # copy per plane), each panel all-gathered as soon as its slice is in
+    works, ready = [], []
+    with (torch.cuda.stream(up) if cuda else _null_ctx()):
+        if cuda:
+            up.wait_stream(comp)  # the zero fills above
+        if rows:
+            dA[:, :rows].copy_(hA, non_blocking=cuda)
+        a_ready = mark(up)
+        for p, (k0, _k1) in enumerate(parts):
+            s0 = k0 + rank * chunk
+            s1 = min(k, s0 + chunk)
+            for w in range(W):
+                if s1 > s0:
+                    piece[p, w, : s1 - s0].copy_(hB[w, s0:s1], non_blocking=cuda)
+            if multi:
+                works.append([dist.all_gather_into_tensor(dB[w, k0:k0 + pk], piece[p, w], group=group,
+                                                          async_op=True) for w in range(W)])
+            else:
+                dB[:, k0:k0 + pk].copy_(piece[p])
+                works.append([])
+            ready.append(mark(up))
+    if a_ready is not None:
+        comp.wait_event(a_ready)
+
+    # the last panel runs in row chunks so the download of C overlaps it
+    tail = [(0, rows)]
+    if cuda and rows >= 128:
+        step = max(64, (rows // 4 + 63) // 64 * 64)
+        tail = [(r, min(rows, r + step)) for r in range(0, rows, step)]
+    launches = 0
+    lda = dA.shape[2]
+    for p, (k0, k1) in enumerate(parts):
+        for wk in works[p]:
+            wk.wait()  # the compute stream waits for this panel only
+        if ready[p] is not None:
+            comp.wait_event(ready[p])
+        if rows == 0:
+            continue
+        if gemm is not None:
+            launches += gemm(W, dA[:, :rows, k0:k1], dB[:, k0:k1], dC, rows, n, k1 - k0, ldc, p > 0)
+            continue
+        f = L.gemm_device if p == 0 else L.gemm_device_acc
+        for r0, r1 in (tail if p == len(parts) - 1 else [(0, rows)]):
+            launches += f(W, r1 - r0, n, k1 - k0, dA.data_ptr() + 8 * (r0 * lda + k0), lda, dA.shape[1] * lda,
+                          dB.data_ptr() + 8 * k0 * ld, ld, dB.shape[1] * ld, dC.data_ptr() + 8 * r0 * ldc, ldc,
+                          dC.shape[1] * ldc, comp.cuda_stream)
+            if p == len(parts) - 1:
+                done = mark(comp)
+                down.wait_event(done)
+                with torch.cuda.stream(down):
+                    for w in range(W):
+                        hC[w, r0:r1].copy_(dC[w, r0:r1], non_blocking=True)
+    if rows and (gemm is not None or not parts):
+        if cuda:
+            down.wait_stream(comp)
+        with (torch.cuda.stream(down) if cuda else _null_ctx()):
+            hC.copy_(dC[:, :rows], non_blocking=cuda)
+    if cuda:
+        comp.synchronize()
+        up.synchronize()
+        down.synchronize()
+    return launches
+
+
+class _null_ctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 class PeerBSlices:
     """B row-sliced across the ranks for the fused all-gather -> GEMM: rank r
     owns rows [cuts[r], cuts[r+1]) in a libmpfk device allocation exported

@@ -49,3 +49,43 @@ def test_torchrun_fused_allgather_path(gpu_lib):
     assert line["check_sharded_equals_one_shot"] is True
     assert line["gpu_launches"] == 2
     assert "fused all-gather" in line["config"]["parallelism"]
+
+
+@pytest.mark.gpu
+def test_torchrun_e2e_host_operands(gpu_lib):
+    """the e2e leg under torchrun: every rank copies its A shard and 1/ws of
+    B from pinned host memory (dist.matmul_sharded_into); its C shard must
+    equal the device-resident run bit for bit."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--workload", "td1024",
+           "--steps", "2", "--warmup", "1", "--no-cpu-baseline", "--dist", "--panels", "4"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    e2e = line["e2e"]
+    assert e2e["matches_device_run"] is True
+    assert e2e["api"].startswith("dist.matmul_sharded_into")
+    assert e2e["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,m,k,n,panels", [(2, 100, 300, 70, 3), (3, 64, 1000, 33, 8), (4, 17, 31, 9, 2)])
+def test_matmul_sharded_into_single_rank(gpu_lib, W, m, k, n, panels):
+    """without a process group: panels copied from the host, continuation
+    GEMMs; bit-identical to matmul_block_into, pads +0."""
+    import torch
+
+    import oracle as O
+    from paper_2101_06584_b200.dist import gather_panels, matmul_sharded_into
+    P = gpu_lib
+    A = P.MPMatrix.from_planes(O.orc_fill_baseline(W, m, k, 5, wide=True)[:, :, :k], pinned=True)
+    B = P.MPMatrix.from_planes(O.orc_fill_baseline(W, k, n, 6, wide=True)[:, :, :n], pinned=True)
+    C1 = P.MPMatrix(W, m, n, pinned=True)
+    C1.data[...] = 3.0
+    launches = matmul_sharded_into(C1, A, B, panels=panels, device=torch.device("cuda", 0))
+    C2 = P.MPMatrix(W, m, n)
+    P.matmul_block_into(C2, A, B)
+    assert P.bits_equal(C1, C2)
+    assert launches == len(gather_panels(k, panels, 1)[1])
+    with pytest.raises(ValueError, match="inner dimensions differ"):
+        matmul_sharded_into(C1, A, P.MPMatrix(W, k + 1, n))

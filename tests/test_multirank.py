@@ -140,3 +140,76 @@ def test_two_rank_gloo_overlapped_k_panels(W, m, k, n):
     same, launches = q.get(timeout=10)
     from paper_2101_06584_b200.dist import k_panels
     assert same and launches == len(k_panels(k, 3)) > 1
+
+
+def _oracle_panel(W_, Ap, Bp, dC_, rows_, n_, kp, ld_, acc):
+    import oracle as O
+    a = np.ascontiguousarray(Ap.numpy())
+    b = np.ascontiguousarray(Bp.numpy())
+    c = np.ascontiguousarray(dC_[:, :rows_].numpy())
+    if not acc:
+        c[...] = O.orc_gemm(a, b, kp, n_)[:, :, : c.shape[2]]
+    else:
+        O.orc().orc_gemm_acc(W_, rows_, kp, n_, a.ctypes.data, a.shape[2], a.shape[1] * a.shape[2],
+                             b.ctypes.data, b.shape[2], b.shape[1] * b.shape[2], c.ctypes.data,
+                             c.shape[2], c.shape[1] * c.shape[2])
+    dC_[:, :rows_] = torch.from_numpy(c)
+    return 1
+
+
+def _worker_host(rank, world, port, W, m, k, n, panels, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle as O
+        from paper_2101_06584_b200 import MPMatrix
+        from paper_2101_06584_b200.dist import matmul_sharded_into
+        Af = O.orc_fill_baseline(W, m, k, 1, wide=True)
+        Bf = O.orc_fill_baseline(W, k, n, 2, wide=True)
+        r0, r1 = shard_rows(m, world, rank, align=8)
+        A = MPMatrix.from_planes(Af[:, r0:r1, :k])
+        B = MPMatrix.from_planes(Bf[:, :, :n])
+        Cs = MPMatrix(W, r1 - r0, n)
+        Cs.data[...] = 7.0  # must be overwritten, pads included
+        launches = matmul_sharded_into(Cs, A, B, panels=panels, device=torch.device("cpu"), gemm=_oracle_panel)
+        Cfull = gather_c(torch.from_numpy(Cs.data), m, world, align=8)
+        if rank == 0:
+            want = O.orc_gemm(Af, Bf, k, n)
+            q.put((np.array_equal(Cfull.numpy().view(np.uint64), want.view(np.uint64)), launches))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("W,m,k,n,panels", [(2, 21, 50, 13, 3), (3, 9, 70, 5, 2), (4, 12, 33, 7, 8),
+                                            (2, 5, 31, 6, 1)])
+def test_two_rank_gloo_host_operands_sliced_b(W, m, k, n, panels):
+    """B starts on the host: each rank uploads 1/2 of every K panel, the
+    panels are all-gathered, the shard GEMM continues panel by panel; the
+    assembled C is bit-identical to the one-shot product, including ragged
+    last panels (k not a multiple of the panel height)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_host, args=(r, 2, port, W, m, k, n, panels, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    same, launches = q.get(timeout=10)
+    from paper_2101_06584_b200.dist import gather_panels
+    assert same and launches == len(gather_panels(k, panels, 2)[1])
+
+
+def test_gather_panels_plan():
+    from paper_2101_06584_b200.dist import gather_panels
+    for k in (1, 15, 16, 100, 8192, 8193):
+        for world in (1, 2, 8):
+            for panels in (1, 3, 8):
+                pk, parts = gather_panels(k, panels, world)
+                assert pk % (16 * world) == 0
+                assert parts[0][0] == 0 and parts[-1][1] == k
+                assert all(b - a <= pk and a % pk == 0 for a, b in parts)
+                assert len(parts) <= panels or pk == 16 * world
+    assert gather_panels(0, 4, 2)[1] == []
