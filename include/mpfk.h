@@ -132,6 +132,28 @@ int mpfk_strassen_device(int width, uint64_t m, uint64_t n, uint64_t k, const do
                          uint64_t cutoff, void *stream, int *launches);
 int mpfk_last_stats(mpfk_stats *out);
 
+/* Flags of mpfk_gemm / mpfk_gemm_device_ex ("flags selects
+ * BIT_EXACT (default) or FAST (reordered, tolerance-checked)").
+ * MPFK_BIT_EXACT: the reference's per-element order; bit-identical to
+ *   linalg::matmul_block_into (linalg.hpp:338-344).
+ * MPFK_FAST: when the bit-exact launch would under-use the GPU (too few
+ *   output tiles for the resident CTA slots, or a badly quantised last wave;
+ *   predicted < 90 %) and k >= 512, K is cut into S segments, each a
+ *   reference-order chain, and the S partial products are added in a fixed
+ *   order (mpf::add<W>); otherwise identical to MPFK_BIT_EXACT.
+ *   Deterministic for a given shape and device; normwise relative error
+ *   within 4*k*u_p (u_p = 2^-104 / 2^-156 / 2^-208). */
+enum mpfk_flags { MPFK_BIT_EXACT = 0u, MPFK_FAST = 1u };
+
+/* The SURVEY's proposed entry point: C = A*B for host matrices in the
+ * reference layout on n_gpus GPUs (<= 0: all visible), rows of C sharded
+ * like matmul_block_parallel_into.  Validation, pads, op counters and
+ * synchronous completion as mpfk_matmul_block_parallel_into; with
+ * MPFK_BIT_EXACT it IS that call (n_min and variant have no effect on the
+ * GPU). */
+int mpfk_gemm(int width, const mpfk_mat *A, const mpfk_mat *B, mpfk_mat *C, int n_gpus,
+              unsigned flags);
+
 /* ---- GEMM, device-resident operands ------------------------------------ */
 
 /* C[0:m,0:n] = A[0:m,0:k] * B[0:k,0:n] on the CURRENT device, enqueued on
@@ -145,6 +167,15 @@ int mpfk_gemm_device(int width, uint64_t m, uint64_t n, uint64_t k, const double
                      uint64_t lda, uint64_t a_plane, const double *B, uint64_t ldb,
                      uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, void *stream,
                      int *launches);
+
+/* mpfk_gemm_device with flags (MPFK_FAST may split K; see mpfk_flags). */
+int mpfk_gemm_device_ex(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                        uint64_t lda, uint64_t a_plane, const double *B, uint64_t ldb,
+                        uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, unsigned flags,
+                        void *stream, int *launches);
+/* the number of K segments MPFK_FAST uses for an m x n x k product on the
+ * current device (1 = the bit-exact path); negative status on error */
+int mpfk_splitk_segments(int width, uint64_t m, uint64_t n, uint64_t k);
 
 /* Continuation over a K panel: C = C (+) A*B, i.e. every element's chain
  * continues with add(C, mul(A(i,k), B(k,j))) for k = 0..k-1 of this panel.

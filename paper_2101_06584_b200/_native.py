@@ -12,6 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmpfk.so")
 
 MPFK_OK, MPFK_EINVAL, MPFK_ERUNTIME, MPFK_ECUDA, MPFK_ENOMEM, MPFK_ENODEV = range(6)
+MPFK_BIT_EXACT, MPFK_FAST = 0, 1  # mpfk_flags
 
 
 class MpfkMat(C.Structure):
@@ -72,6 +73,11 @@ _SIGS = {
     "mpfk_last_stats": (C.c_int, [C.POINTER(MpfkStats)]),
     "mpfk_gemm_device": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                    _U64, _P, C.POINTER(C.c_int)]),
+    "mpfk_gemm": (C.c_int, [C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat), C.POINTER(MpfkMat), C.c_int,
+                            C.c_uint]),
+    "mpfk_gemm_device_ex": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
+                                      _U64, C.c_uint, _P, C.POINTER(C.c_int)]),
+    "mpfk_splitk_segments": (C.c_int, [C.c_int, _U64, _U64, _U64]),
     "mpfk_ew_apply_into": (C.c_int, [C.c_int, C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat),
                                      C.POINTER(MpfkMat), C.c_int]),
     "mpfk_ew_device": (C.c_int, [C.c_int, C.c_int, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64,

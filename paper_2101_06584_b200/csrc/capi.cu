@@ -26,6 +26,7 @@
 #include "../../include/mpfk.h"
 #include "ew_kernel.cuh"
 #include "gemm_kernel.cuh"
+#include "splitk.cuh"
 #include "strassen_kernels.cuh"
 #include "mpf_arith.cuh"
 
@@ -270,14 +271,18 @@ long long tiles_of(const kern::GemmArgs& g) {
 // (measured by the sweep) times the per-SM balance of the tile count -- the
 // FP64 pipe is shared by all CTAs resident on an SM, so what quantises is
 // tiles per SM (tiles / SMs vs its ceiling), e.g. DD n=1024: 256 64x64 tiles
-// -> 1.73 per SM (0.86), 1024 32x32 tiles -> 6.92 per SM (0.99).
+// -> 1.73 per SM (0.86), 1024 32x32 tiles -> 6.92 per SM (0.99) -- times the
+// share of tile cells inside the m x n output.
 template <class Cfg>
 double predicted_eff(const kern::GemmArgs& g, double steady) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const double per_sm = double(tiles_of<Cfg>(g)) / std::max(sms, 1);
-  return steady * per_sm / std::ceil(per_sm);
+  // cells of the tiles that hold output (edge tiles compute masked cells too)
+  const double useful = double(g.M) * g.N /
+                        (double((g.M + Cfg::BM - 1) / Cfg::BM * Cfg::BM) * ((g.N + Cfg::BN - 1) / Cfg::BN * Cfg::BN));
+  return steady * useful * per_sm / std::ceil(per_sm);
 }
 
 template <class Cfg>
@@ -379,6 +384,38 @@ int dispatch_gemm_pull(int W, const kern::GemmArgs& g, const kern::PullB& P, cud
   return 1;
 }
 
+template <class Cfg>
+void launch_splitk_cfg(const kern::GemmArgs& g, int klast, cudaStream_t s) {
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    ck(cudaFuncSetAttribute(kern::mpgemm_splitk_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)Cfg::SMEM),
+       "cudaFuncSetAttribute");
+    configured_dev = dev;
+  }
+  const long long tiles = tiles_of<Cfg>(g);
+  if (tiles > 0x7fffffffLL) fail(MPFK_EINVAL, "mpfk: too many tiles");
+  kern::mpgemm_splitk_kernel<Cfg><<<(unsigned)tiles, Cfg::THREADS, Cfg::SMEM, s>>>(g, klast);
+  ck(cudaGetLastError(), "split-K GEMM launch");
+}
+
+int dispatch_gemm_splitk(int W, const kern::GemmArgs& g, int klast, cudaStream_t s) {
+  switch (W) {
+    case 2:
+      if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
+        launch_splitk_cfg<Cfg2s>(g, klast, s);
+      else
+        launch_splitk_cfg<Cfg2>(g, klast, s);
+      break;
+    case 3: launch_splitk_cfg<Cfg3>(g, klast, s); break;
+    case 4: launch_splitk_cfg<Cfg4>(g, klast, s); break;
+    default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
+  }
+  return 1;
+}
+
 int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s) {
   switch (W) {
     case 2:
@@ -392,6 +429,81 @@ int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s) {
     default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
   }
   return 1;
+}
+
+// ---------------------------------------------------------------------------
+// MPFK_FAST: split-K (csrc/splitk.cuh)
+// ---------------------------------------------------------------------------
+struct SplitK {
+  int S;        // K segments (1 = the bit-exact path)
+  uint64_t ks;  // segment length (multiple of 16: 16-byte A offsets)
+};
+
+// Split K only when the bit-exact launch would leave the GPU under-used
+// (predicted efficiency < 0.9: fewer tiles than resident CTA slots, or a
+// badly quantised last wave) and k >= 512.  The segment count is the
+// smallest whose tiles-per-SM balance x slot occupancy reaches 0.98 (else
+// the best), with segments of >= 256 k steps and at most 4096 segments.
+SplitK splitk_plan(int W, uint64_t m, uint64_t n, uint64_t k) {
+  int BM = Cfg2s::BM, BN = Cfg2s::BN, minb = Cfg2s::MINB;
+  if (W == 3) BM = Cfg3::BM, BN = Cfg3::BN, minb = Cfg3::MINB;
+  if (W == 4) BM = Cfg4::BM, BN = Cfg4::BN, minb = Cfg4::MINB;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const double tiles = double((m + BM - 1) / BM) * double((n + BN - 1) / BN);
+  auto eff = [&](double segs) {
+    const double per_sm = tiles * segs / sms;
+    return per_sm / std::ceil(per_sm) * std::min(1.0, per_sm / minb);
+  };
+  if (m == 0 || n == 0 || k < 512 || eff(1) >= 0.9) return {1, k};
+  const uint64_t smax = std::min<uint64_t>(k / 256, 4096);
+  SplitK best{1, k};
+  double best_eff = eff(1);
+  for (uint64_t S = 2; S <= smax; ++S) {
+    const uint64_t ks = ((k + S - 1) / S + 15) / 16 * 16;
+    const uint64_t segs = (k + ks - 1) / ks;
+    const double e = eff((double)segs);
+    if (e > best_eff + 1e-9) best_eff = e, best = {(int)segs, ks};
+    if (best_eff >= 0.98) break;
+  }
+  return best;
+}
+
+// C = A*B with MPFK_FAST on the current device: split-K when the plan says
+// so (one batched GEMM launch over the segments + one combine launch, the
+// partials in stream-ordered scratch), else exactly enqueue_gemm.
+int enqueue_gemm_fast(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                      uint64_t pa, const double* B, uint64_t ldb, uint64_t pb, double* C,
+                      uint64_t ldc, uint64_t pc, cudaStream_t s) {
+  const SplitK p = splitk_plan(W, m, n, k);
+  if (p.S <= 1) return enqueue_gemm(W, m, n, k, A, lda, pa, B, ldb, pb, C, ldc, pc, s);
+  if (m > 0x7fffffffULL || n > 0x7fffffffULL || k > 0x7fffffffULL)
+    fail(MPFK_EINVAL, "mpfk: dimension exceeds 2^31-1");
+  const uint64_t ldw = (n + 1) & ~uint64_t(1), pw = m * ldw, sw = W * pw;
+  double* ws = nullptr;
+  ck(cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(double) * sw * p.S, s), "split-K scratch");
+  kern::GemmArgs g;
+  g.A = A, g.B = B, g.C = ws;
+  g.lda = (long long)lda, g.ldb = (long long)ldb, g.ldc = (long long)ldw;
+  g.pa = (long long)pa, g.pb = (long long)pb, g.pc = (long long)pw;
+  g.M = (int)m, g.N = (int)n, g.K = (int)p.ks;
+  g.accumulate = 0;
+  g.batch = p.S, g.sa = (long long)p.ks, g.sb = (long long)(p.ks * ldb), g.sc = (long long)sw;
+  const uint64_t klast = k - (uint64_t)(p.S - 1) * p.ks;
+  int launches = dispatch_gemm_splitk(W, g, klast == p.ks ? 0 : (int)klast, s);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m * n + 255) / 256, (uint64_t)sms * 8));
+  switch (W) {
+    case 2: kern::splitk_reduce_kernel<2><<<blocks, 256, 0, s>>>(ws, ldw, pw, sw, p.S, C, ldc, pc, (int)m, (int)n); break;
+    case 3: kern::splitk_reduce_kernel<3><<<blocks, 256, 0, s>>>(ws, ldw, pw, sw, p.S, C, ldc, pc, (int)m, (int)n); break;
+    default: kern::splitk_reduce_kernel<4><<<blocks, 256, 0, s>>>(ws, ldw, pw, sw, p.S, C, ldc, pc, (int)m, (int)n); break;
+  }
+  ck(cudaGetLastError(), "split-K combine launch");
+  ck(cudaFreeAsync(ws, s), "split-K scratch free");
+  return launches + 1;
 }
 
 // Enqueue out = op(a, b) elementwise on the current device.
@@ -488,7 +600,9 @@ struct Shard {
 
 // The multi-GPU host-buffer GEMM.  Device layout: planes packed with
 // ld = pad4(cols) (16-byte rows for cp.async), A shard rows only, full B.
-void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigned gpus) {
+// fast: MPFK_FAST -- shards whose output cannot fill the GPU take the
+// split-K path (enqueue_gemm_fast); everything else is bit-exact.
+void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigned gpus, bool fast = false) {
   std::lock_guard<std::mutex> call_lock(g_call_mu);
   const auto t0 = std::chrono::steady_clock::now();
   const uint64_t m = A->rows, K = A->cols, n = B->cols;
@@ -633,7 +747,11 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
       cudaStream_t cs = (c & 1) ? D.stream2 : D.stream;
       const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
       ck(cudaStreamWaitEvent(cs, D.evA[c], 0), "wait A chunk");
-      if (c == 0 && np > 1) {
+      if (fast && splitk_plan(W, c1 - c0, n, K).S > 1) {
+        ck(cudaStreamWaitEvent(cs, b_ready, 0), "wait B");
+        launches[g] += enqueue_gemm_fast(W, c1 - c0, n, K, D.dA + c0 * lda, lda, rows * lda, D.dB, ldb,
+                                         K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs);
+      } else if (c == 0 && np > 1) {
         for (int p = 0; p < np; ++p) {
           const uint64_t k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
           ck(cudaStreamWaitEvent(cs, D.evB[p], 0), "wait B panel");
@@ -1031,6 +1149,54 @@ int mpfk_gemm_device(int width, uint64_t m, uint64_t n, uint64_t k, const double
     count_matmul(m, n, k);
     if (launches) *launches = l;
   });
+}
+
+int mpfk_gemm(int width, const mpfk_mat* A, const mpfk_mat* B, mpfk_mat* C, int n_gpus, unsigned flags) {
+  return guarded([&] {
+    check_width(width);
+    check_mat(A, "A");
+    check_mat(B, "B");
+    check_mat(C, "C");
+    check_mul_shapes(A, B, C);
+    if (flags & ~unsigned(MPFK_FAST)) fail(MPFK_EINVAL, "mpfk: unknown flags");
+    unsigned gpus = n_gpus > 0 ? (unsigned)n_gpus : (unsigned)std::max(1, visible_sm100_devices());
+    host_gemm(width, C, A, B, gpus, (flags & MPFK_FAST) != 0);
+  });
+}
+
+int mpfk_gemm_device_ex(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                        uint64_t a_plane, const double* B, uint64_t ldb, uint64_t b_plane, double* C,
+                        uint64_t ldc, uint64_t c_plane, unsigned flags, void* stream, int* launches) {
+  return guarded([&] {
+    check_width(width);
+    if (flags & ~unsigned(MPFK_FAST)) fail(MPFK_EINVAL, "mpfk: unknown flags");
+    if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
+    if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
+      fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+         reinterpret_cast<uintptr_t>(C)) & 15)
+      fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int l = (flags & MPFK_FAST) ? enqueue_gemm_fast(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc,
+                                                          c_plane, s)
+                                      : enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc,
+                                                     c_plane, s);
+    count_matmul(m, n, k);
+    if (launches) *launches = l;
+  });
+}
+
+int mpfk_splitk_segments(int width, uint64_t m, uint64_t n, uint64_t k) {
+  int segs = 1;
+  const int rc = guarded([&] {
+    check_width(width);
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    segs = splitk_plan(width, m, n, k).S;
+  });
+  return rc == MPFK_OK ? segs : -rc;
 }
 
 int mpfk_ew_apply_into(int width, int op, mpfk_mat* out, const mpfk_mat* a, const mpfk_mat* b,

@@ -250,7 +250,7 @@ __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W]
 }
 
 template <class Cfg, bool kPull>
-__device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P) {
+__device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, int klast = 0) {
   constexpr int W = Cfg::W, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, TX = Cfg::TX, TY = Cfg::TY;
   constexpr int STAGES = Cfg::STAGES;
@@ -266,6 +266,7 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P) {
     lin -= bz * tiles_m * tiles_n;
   }
   GemmArgs g = g0;
+  if (klast && bz == g0.batch - 1) g.K = klast;  // split-K: ragged last segment
   g.A += bz * g0.sa;
   g.B += bz * g0.sb;
   g.C += bz * g0.sc;
@@ -372,6 +373,14 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P) {
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_kernel(const GemmArgs g0) {
   gemm_body<Cfg, false>(g0, PullB{});
+}
+
+// MPFK_FAST split-K (csrc/splitk.cuh): the batch is the K segments, the
+// last one running over klast k steps (a separate kernel so the product
+// kernels keep their code generation).
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_splitk_kernel(const GemmArgs g0, int klast) {
+  gemm_body<Cfg, false>(g0, PullB{}, klast);
 }
 
 // The fused all-gather -> GEMM (see PullB); batch must be 1.

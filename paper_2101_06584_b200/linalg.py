@@ -187,6 +187,32 @@ def matmul_naive_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix,
     N.check(N.lib().mpfk_matmul_naive_into(W, C.byref(c), C.byref(a), C.byref(b), int(variant)))
 
 
+BIT_EXACT, FAST = N.MPFK_BIT_EXACT, N.MPFK_FAST
+
+
+def gemm_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix, n_gpus: int = 1, flags: int = BIT_EXACT):
+    """mpfk_gemm: C = A*B on n_gpus GPUs (<= 0: all).  flags=BIT_EXACT is
+    matmul_block_parallel_into; flags=FAST may split K for outputs too small
+    to fill the GPU (deterministic, tolerance-checked: normwise 4*k*u_p)."""
+    W = _check_same_width(C_, A, B)
+    c, a, b = C_._c(), A._c(), B._c()
+    N.check(N.lib().mpfk_gemm(W, C.byref(a), C.byref(b), C.byref(c), int(n_gpus), int(flags)))
+
+
+def gemm(A: MPMatrix, B: MPMatrix, n_gpus: int = 1, flags: int = BIT_EXACT, pinned: bool = False) -> MPMatrix:
+    C_ = MPMatrix(A.W, A.rows(), B.cols(), pinned=pinned)
+    gemm_into(C_, A, B, n_gpus, flags)
+    return C_
+
+
+def splitk_segments(W: int, m: int, n: int, k: int) -> int:
+    """K segments FAST uses for an m x n x k product here (1 = bit-exact)."""
+    r = N.lib().mpfk_splitk_segments(W, m, n, k)
+    if r < 0:
+        N.check(-r)
+    return r
+
+
 def matmul_block_parallel(A: MPMatrix, B: MPMatrix, n_min: int = 32,
                           variant: KernelVariant = KernelVariant.NORMAL, workers: int = 1,
                           pinned: bool = False) -> MPMatrix:
@@ -315,6 +341,15 @@ def gemm_device(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: i
     launches = C.c_int(0)
     N.check(N.lib().mpfk_gemm_device(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
                                      c_plane, stream or None, C.byref(launches)))
+    return launches.value
+
+
+def gemm_device_ex(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int, ldb: int,
+                   b_plane: int, C_ptr: int, ldc: int, c_plane: int, flags: int = BIT_EXACT, stream: int = 0) -> int:
+    """mpfk_gemm_device_ex: gemm_device with flags (FAST may split K)."""
+    launches = C.c_int(0)
+    N.check(N.lib().mpfk_gemm_device_ex(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
+                                        c_plane, int(flags), stream or None, C.byref(launches)))
     return launches.value
 
 
