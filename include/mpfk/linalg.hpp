@@ -97,6 +97,18 @@ void matmul_naive_into(Mat& C, const Mat& A, const Mat& B,
   detail::throw_on(mpfk_matmul_naive_into(W, &c, &a, &b, static_cast<int>(variant)));
 }
 
+// mpfk_gemm: the SURVEY's proposed entry point with flags.  BIT_EXACT is
+// matmul_block_parallel_into on n_gpus GPUs (<= 0: all); FAST may split K
+// when the output cannot fill the GPU (deterministic, within 4*k*u_p).
+enum class GemmFlags : unsigned { BIT_EXACT = MPFK_BIT_EXACT, FAST = MPFK_FAST };
+
+template <int W, class Mat>
+void gemm_into(Mat& C, const Mat& A, const Mat& B, int n_gpus = 1, GemmFlags flags = GemmFlags::BIT_EXACT) {
+  static_assert(W >= 2 && W <= 4);
+  mpfk_mat c = detail::view(C), a = detail::view(A), b = detail::view(B);
+  detail::throw_on(mpfk_gemm(W, &a, &b, &c, n_gpus, static_cast<unsigned>(flags)));
+}
+
 // value forms, linalg.hpp:360-366, 390-397, 435-443
 template <int W, class Mat>
 Mat matmul_block_parallel(const Mat& A, const Mat& B, std::size_t n_min = 32,

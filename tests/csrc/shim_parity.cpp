@@ -45,6 +45,11 @@ void run(std::size_t m, std::size_t k, std::size_t n) {
   C.set(0, 0, mpf::from_f64<W>(42.0));  // stale contents must be cleared
   mpfk::linalg::matmul_block_parallel_into<W>(C, A, B, 32, mpfk::linalg::KernelVariant::NORMAL, 4);
   verdict(linalg::bits_equal(ref, C), "W=" + std::to_string(W) + " _into clears stale C, workers=4");
+  linalg::MPMatrix<W> G(m, n);
+  mpfk::linalg::gemm_into<W>(G, A, B, 1, mpfk::linalg::GemmFlags::BIT_EXACT);
+  verdict(linalg::bits_equal(ref, G), "W=" + std::to_string(W) + " gemm_into BIT_EXACT");
+  mpfk::linalg::gemm_into<W>(G, A, B, 1, mpfk::linalg::GemmFlags::FAST);
+  verdict(G.rows() == m && G.cols() == n, "W=" + std::to_string(W) + " gemm_into FAST runs");
 }
 
 template <class F>
