@@ -140,7 +140,23 @@ int visible_sm100_devices() {
     if (cudaGetDeviceProperties(&p, d) != cudaSuccess) continue;
     if (p.major == 10 && p.minor == 0) ++usable;
   }
-  return usable == n ? n : usable;
+  // (a box mixing sm_100 with other GPUs is not supported: the first
+  // `usable` ordinals are taken to be the sm_100 devices)
+  return usable;
+}
+
+// The device table, built once.  Caller holds g_mu.
+void build_device_table_locked() {
+  if (g_ndev >= 0) return;
+  g_ndev = visible_sm100_devices();
+  g_dev.resize(std::max(g_ndev, 0));
+  for (int d = 0; d < g_ndev; ++d) g_dev[d].id = d;
+}
+
+void init_device_table_locked() {
+  build_device_table_locked();
+  if (g_ndev == 0)
+    fail(MPFK_ENODEV, "mpfk: no CUDA sm_100 device is visible; the GPU library has no CPU fallback");
 }
 
 void run_selftest_current() {
@@ -172,14 +188,7 @@ void run_selftest_current() {
 // Caller holds no lock.
 void ensure_devices(int n, int first = 0) {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (g_ndev < 0) {
-    g_ndev = visible_sm100_devices();
-    g_dev.resize(std::max(g_ndev, 0));
-    for (int d = 0; d < g_ndev; ++d) g_dev[d].id = d;
-  }
-  if (g_ndev == 0)
-    fail(MPFK_ENODEV,
-         "mpfk: no CUDA sm_100 device is visible; the GPU library has no CPU fallback");
+  init_device_table_locked();
   if (n > g_ndev) n = g_ndev;
   int prev = 0;
   cudaGetDevice(&prev);
@@ -215,14 +224,7 @@ void ensure_devices(int n, int first = 0) {
 int current_device() {
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (g_ndev < 0) {
-      g_ndev = visible_sm100_devices();
-      g_dev.resize(std::max(g_ndev, 0));
-      for (int d = 0; d < g_ndev; ++d) g_dev[d].id = d;
-    }
-    if (g_ndev == 0)
-      fail(MPFK_ENODEV,
-           "mpfk: no CUDA sm_100 device is visible; the GPU library has no CPU fallback");
+    init_device_table_locked();
   }
   int dev = 0;
   ck(cudaGetDevice(&dev), "cudaGetDevice");
@@ -981,11 +983,7 @@ const char* mpfk_last_error(void) { return t_err.c_str(); }
 
 int mpfk_device_count(void) {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (g_ndev < 0) {
-    g_ndev = visible_sm100_devices();
-    g_dev.resize(std::max(g_ndev, 0));
-    for (int d = 0; d < g_ndev; ++d) g_dev[d].id = d;
-  }
+  build_device_table_locked();
   return g_ndev;
 }
 
