@@ -1157,8 +1157,8 @@ int mpfk_gemm(int width, const mpfk_mat* A, const mpfk_mat* B, mpfk_mat* C, int 
     check_mat(C, "C");
     check_mul_shapes(A, B, C);
     if (flags & ~unsigned(MPFK_FAST)) fail(MPFK_EINVAL, "mpfk: unknown flags");
-    unsigned gpus = n_gpus > 0 ? (unsigned)n_gpus : (unsigned)std::max(1, visible_sm100_devices());
-    host_gemm(width, C, A, B, gpus, (flags & MPFK_FAST) != 0);
+    // n_gpus <= 0: every visible device (host_gemm caps the count)
+    host_gemm(width, C, A, B, n_gpus > 0 ? (unsigned)n_gpus : 1u << 20, (flags & MPFK_FAST) != 0);
   });
 }
 
