@@ -67,16 +67,15 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>}
 
 const Entry kEntries[] = {
-    F(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 0),
-    F(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 1),
-    F(2, 64, 64, 16, 4, 4, 2, 4, 16, 2, 1),
-    F(2, 64, 64, 16, 4, 4, 2, 1, 16, 2, 1),
-    F(3, 32, 32, 16, 2, 2, 2, 1, 16, 3, 0),
-    F(3, 32, 32, 16, 2, 2, 2, 1, 16, 3, 1),
-    F(3, 32, 32, 16, 2, 2, 2, 2, 16, 3, 1),
-    F(4, 16, 32, 16, 1, 2, 2, 1, 16, 3, 0),
-    F(4, 16, 32, 16, 1, 2, 2, 1, 16, 3, 1),
-    F(4, 16, 32, 16, 1, 2, 2, 2, 16, 3, 1),
+    E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // product, large
+    E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // product, few waves
+    E(2, 32, 32, 16, 4, 4, 2, 2, 16, 6),  // 64 threads
+    E(2, 32, 32, 8, 4, 4, 2, 2, 16, 8),
+    E(2, 32, 32, 16, 4, 4, 2, 2, 16, 4),
+    E(2, 64, 32, 16, 4, 4, 2, 2, 16, 4),  // 128 threads
+    E(2, 32, 64, 16, 4, 4, 2, 2, 16, 4),
+    E(2, 64, 32, 16, 4, 4, 2, 2, 16, 3),
+    E(2, 32, 64, 8, 4, 4, 2, 2, 16, 4),
 };
 }  // namespace
 
