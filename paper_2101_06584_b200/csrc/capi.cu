@@ -664,13 +664,39 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   // Row chunks of each shard are pipelined over three streams: H2D of chunk
   // c+1 (copy engine) and D2H of chunk c-1 (second copy engine) overlap the
   // GEMM of chunk c.  Rows of C are independent, so chunking cannot change a
-  // bit.  A chunk is sized to keep >= 4 tiles per SM per launch.
-  auto chunks_of = [&](uint64_t rows) {
-    const double tiles_per_row = double(n) / (64.0 * 64.0);
-    const uint64_t min_rows = (uint64_t)std::ceil(148.0 * 4.0 / std::max(tiles_per_row, 1e-9));
-    uint64_t nc = std::max<uint64_t>(1, std::min<uint64_t>(kMaxChunks, rows / std::max<uint64_t>(min_rows, 1)));
+  // bit.  A chunk is sized to keep >= 4 64x64 tiles per SM per launch.  A
+  // shard too small for two such chunks is cut into chunks that each fill
+  // one wave of resident CTAs of the small-tile configuration; failing that,
+  // into chunks of >= 1.5 small tiles per SM (the two compute streams fill
+  // each other's tails) only when the copies are a large share of the work
+  // (DD: 20 FP64 ops per MAC; TD/QD do 6-11x more per byte).  Measured on
+  // DD/TD/QD n=1024.
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, base);
+  int sBM = Cfg2s::BM, sBN = Cfg2s::BN, sMINB = Cfg2s::MINB;
+  if (W == 3) sBM = Cfg3::BM, sBN = Cfg3::BN, sMINB = Cfg3::MINB;
+  if (W == 4) sBM = Cfg4::BM, sBN = Cfg4::BN, sMINB = Cfg4::MINB;
+  auto split = [](uint64_t rows, uint64_t min_rows) {
+    const uint64_t nc = std::max<uint64_t>(1, std::min<uint64_t>(kMaxChunks, rows / std::max<uint64_t>(min_rows, 1)));
     const uint64_t crows = ((rows + nc - 1) / nc + 63) / 64 * 64;
     return std::make_pair((rows + crows - 1) / std::max<uint64_t>(crows, 1), crows);
+  };
+  auto chunks_of = [&](uint64_t rows) {
+    const double big = double(n) / (64.0 * 64.0);
+    const uint64_t min_rows = (uint64_t)std::ceil(sms * 4.0 / std::max(big, 1e-9));
+    if (rows >= 2 * min_rows) return split(rows, min_rows);
+    // chunks that each fill one wave of resident CTAs
+    const uint64_t tiles_per_band = (n + sBN - 1) / sBN;
+    const uint64_t wave_rows = (uint64_t(sms) * sMINB + tiles_per_band - 1) / tiles_per_band * sBM;
+    const auto wave = split(rows, wave_rows);
+    if (wave.first >= 2) return wave;
+    // under-filled chunks only when the copies are a large share
+    const double ops = W == 2 ? 20.0 : W == 3 ? 132.0 : 218.0;
+    const double copy_s = 8.0 * W * double(rows * K + K * n + rows * n) / 50e9;  // ~PCIe 5 x16
+    const double kern_s = double(rows) * n * K * ops / 18e12;                    // ~FP64 peak
+    if (copy_s > 0.3 * kern_s)
+      return split(rows, (uint64_t)std::ceil(sms * 1.5 / std::max(double(tiles_per_band) / sBM, 1e-9)));
+    return split(rows, rows);
   };
   // Single GPU: B is uploaded in K panels right after the first A chunk, and
   // the first chunk's GEMM runs panel by panel (continuing the chains from C,
