@@ -399,7 +399,7 @@ def run_mpfk(args, ws, rank, local):
         ops = OPS_PER_MAC[W]
         # dominant kernel (the GEMM) of rank 0's shard: algorithmic FP64 ops / launch time
         achieved = rows * n * k * ops / (t_kern * 1e-3) / 1e9  # Gop/s
-        traffic = load_traffic(args.workload)
+        traffic = load_traffic(args.workload) if ws == 1 else None  # captured on the 1-GPU launch
         parallelism = f"row-shard x{ws}"
         if slices is not None:
             parallelism += " + fused all-gather->GEMM (B pulled over peer memory inside the GEMM kernel)"
@@ -433,7 +433,11 @@ def run_mpfk(args, ws, rank, local):
                          "ops_per_mac": ops, "kernel_ms": round(t_kern, 3),
                          "peak_source": "measured on this GPU by mpfk_fp64_peak (DFMA chains); "
                                         "MEASURED_PEAKS.json has no FP64 entry",
-                         "traffic": traffic},
+                         "traffic": traffic,
+                         # the bound is the FP64 pipe: DRAM traffic (L2 re-reads of B across
+                         # tile bands) vs the compulsory bytes, and the HBM rate it implies
+                         "compulsory_bytes": 8 * W * (rows * k + k * n + rows * n),
+                         "traffic_gbs": round(traffic / (t_kern * 1e-3) / 1e9, 1) if traffic else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches[0],
