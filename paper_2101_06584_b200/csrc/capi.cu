@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -146,11 +147,19 @@ int visible_sm100_devices() {
 }
 
 // The device table, built once.  Caller holds g_mu.
+// Testing hook: MPFK_EMULATED_DEVICES=N presents N logical devices that all
+// live on physical device 0 (Device::id is the physical ordinal), so the
+// multi-GPU host path -- row shards, B slices gathered with peer copies, one
+// host thread per device -- runs on a one-GPU box.  The "peer" copies are
+// then device-local copies ordered by events; no kernel waits on another.
 void build_device_table_locked() {
   if (g_ndev >= 0) return;
-  g_ndev = visible_sm100_devices();
-  g_dev.resize(std::max(g_ndev, 0));
-  for (int d = 0; d < g_ndev; ++d) g_dev[d].id = d;
+  const int phys = visible_sm100_devices();
+  const char* emu = std::getenv("MPFK_EMULATED_DEVICES");
+  const int n = (phys > 0 && emu && std::atoi(emu) > 0) ? std::atoi(emu) : phys;
+  g_ndev = n;
+  g_dev.resize(std::max(n, 0));
+  for (int d = 0; d < n; ++d) g_dev[d].id = n == phys ? d : 0;
 }
 
 void init_device_table_locked() {
@@ -196,7 +205,7 @@ void ensure_devices(int n, int first = 0) {
     const int d = (first + i) % g_ndev;
     Device& D = g_dev[d];
     if (D.ready) continue;
-    ck(cudaSetDevice(d), "cudaSetDevice");
+    ck(cudaSetDevice(D.id), "cudaSetDevice");
     run_selftest_current();
     ck(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&D.up, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -210,7 +219,7 @@ void ensure_devices(int n, int first = 0) {
     // keep stream-ordered scratch (Strassen levels) mapped between calls
     // instead of returning it to the OS at every synchronisation
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+    if (cudaDeviceGetDefaultMemPool(&pool, D.id) == cudaSuccess) {
       uint64_t keep = ~uint64_t(0);
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
@@ -642,13 +651,15 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   if (peer) {
     std::lock_guard<std::mutex> lk(g_mu);
     for (int a = 0; a < G; ++a) {
-      ck(cudaSetDevice(sh[a].dev), "cudaSetDevice");
+      const int pa = g_dev[sh[a].dev].id;
+      ck(cudaSetDevice(pa), "cudaSetDevice");
       for (int b = 0; b < G; ++b) {
-        if (a == b) continue;
+        const int pb = g_dev[sh[b].dev].id;
+        if (pa == pb) continue;  // (emulated devices share one GPU)
         int can = 0;
-        cudaDeviceCanAccessPeer(&can, sh[a].dev, sh[b].dev);
+        cudaDeviceCanAccessPeer(&can, pa, pb);
         if (!can) fail(MPFK_ECUDA, "mpfk: GPUs lack peer access for the B all-gather");
-        cudaError_t e = cudaDeviceEnablePeerAccess(sh[b].dev, 0);
+        cudaError_t e = cudaDeviceEnablePeerAccess(pb, 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "enable peer");
         cudaGetLastError();
       }
@@ -672,7 +683,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   // (DD: 20 FP64 ops per MAC; TD/QD do 6-11x more per byte).  Measured on
   // DD/TD/QD n=1024.
   int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, base);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_dev[base].id);
   int sBM = Cfg2s::BM, sBN = Cfg2s::BN, sMINB = Cfg2s::MINB;
   if (W == 3) sBM = Cfg3::BM, sBN = Cfg3::BN, sMINB = Cfg3::MINB;
   if (W == 4) sBM = Cfg4::BM, sBN = Cfg4::BN, sMINB = Cfg4::MINB;
@@ -711,7 +722,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   auto phase1 = [&](int g) {  // allocate; upload A chunk 0, B (slice or K panels), other A chunks
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
-    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaSetDevice(D.id), "cudaSetDevice");
     const uint64_t rows = s.r1 - s.r0;
     grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(rows * lda, 1));
     grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
@@ -749,7 +760,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   auto phase2 = [&](int g) {  // gather B slices from peers, compute chunks, download chunks
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
-    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaSetDevice(D.id), "cudaSetDevice");
     const uint64_t rows = s.r1 - s.r0;
     ck(cudaEventRecord(D.ev[2], D.stream), "event");
     if (peer) {
@@ -759,8 +770,8 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
         Device& P = g_dev[sh[o].dev];
         ck(cudaStreamWaitEvent(D.stream, P.ev[1], 0), "wait peer upload");
         for (int w = 0; w < W; ++w)
-          ck(cudaMemcpyPeerAsync(D.dB + w * K * ldb + sh[o].b0 * ldb, s.dev,
-                                 P.dB + w * K * ldb + sh[o].b0 * ldb, sh[o].dev,
+          ck(cudaMemcpyPeerAsync(D.dB + w * K * ldb + sh[o].b0 * ldb, D.id,
+                                 P.dB + w * K * ldb + sh[o].b0 * ldb, P.id,
                                  (sh[o].b1 - sh[o].b0) * ldb * 8, D.stream),
              "peer copy B");
       }
@@ -1049,7 +1060,12 @@ int mpfk_set_device(int dev) {
     const int n = mpfk_device_count();
     if (n == 0) fail(MPFK_ENODEV, "mpfk: no CUDA sm_100 device is visible; the GPU library has no CPU fallback");
     if (dev < 0 || dev >= n) fail(MPFK_EINVAL, "mpfk: device index out of range");
-    ck(cudaSetDevice(dev), "cudaSetDevice");
+    int phys = dev;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      phys = g_dev[dev].id;
+    }
+    ck(cudaSetDevice(phys), "cudaSetDevice");
     ensure_devices(1, dev);
   });
 }
