@@ -173,6 +173,18 @@ class CpuReference:
         return 2.0 * rows * self.n * self.n / t / 1e9, t, rows
 
 
+def cpu_model():
+    """The host CPU model (report the core count and CPU model)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or None
+
+
 def run_reference(args, ws, rank):
     W, n, wide = WORKLOADS[args.workload]
     if rank != 0:
@@ -204,6 +216,7 @@ def run_reference(args, ws, rank):
         "config": {"workload": args.workload, "precision": NAMES[W], "m": n, "n": n, "k": n,
                    "inputs": "wide 2^[-30,30]" if wide else "U[-1,1)"},
         "cpu_baseline": {"value": round(v, 4), "unit": "Gflop/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{rows} of {n} rows of C per step (rows are independent), "
                                    "mpfkit matmul_block_parallel_into(n_min=32, SIMD_LOADSTORE, "
                                    f"workers={threads}), AVX2 build of /root/reference/proj"},
@@ -389,7 +402,7 @@ def run_mpfk(args, ws, rank, local):
             ref = CpuReference(W, n, wide)
             g, s, srows = ref.measure(args.cpu_seconds)
             thr = ref.threads
-            cpu = {"value": round(g, 4), "unit": "Gflop/s", "cores": thr, "kind": "reference",
+            cpu = {"value": round(g, 4), "unit": "Gflop/s", "cores": thr, "kind": "reference", "cpu_model": cpu_model(),
                    "sample": f"{srows} of {n} rows of C ({s:.1f} s), mpfkit matmul_block_parallel_into"
                              f"(n_min=32, SIMD_LOADSTORE, workers={thr}), AVX2 build of the reference"}
         except Exception as e:  # the checker is optional; the GPU number stands alone
