@@ -15,10 +15,13 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -101,6 +104,176 @@ __global__ void selftest_kernel(const double* in, int* ok) {
 
 constexpr int kMaxChunks = 8;
 
+// ---------------------------------------------------------------------------
+// pageable host buffers (e.g. the reference's aligned_alloc'd MPMatrix): a
+// ring of pinned staging slots filled and drained by a pool of copy threads,
+// so the DMA of one slot overlaps the CPU copy of the next and the calling
+// thread never sits in the driver's single-threaded staging path.
+// ---------------------------------------------------------------------------
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// persistent workers running one job at a time: f(worker, workers)
+class CopyPool {
+ public:
+  explicit CopyPool(int n) : n_(n) {
+    for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void run(const std::function<void(int, int)>& f) {
+    std::unique_lock<std::mutex> lk(mu_);
+    job_ = &f;
+    pending_ = n_;
+    ++gen_;
+    cv_.notify_all();
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      const auto* f = job_;
+      lk.unlock();
+      (*f)(i, n_);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int, int)>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
+// rows x width bytes between two pitched host regions, split over the pool
+void copy_rows(CopyPool& pool, char* dst, size_t dpitch, const char* src, size_t spitch, size_t width,
+               size_t rows) {
+  if (rows * width < (size_t(1) << 20)) {  // small: not worth waking the pool
+    for (size_t r = 0; r < rows; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, width);
+    return;
+  }
+  pool.run([&](int i, int n) {
+    const size_t r0 = rows * i / n, r1 = rows * (i + 1) / n;
+    for (size_t r = r0; r < r1; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, width);
+  });
+}
+
+struct Stager {
+  static constexpr int kSlots = 8;
+  static constexpr size_t kSlotBytes = size_t(16) << 20;
+  char* slot[kSlots] = {};
+  cudaEvent_t ev[kSlots] = {};
+  struct Out {  // a finished-or-in-flight download still to be copied out
+    bool pending = false;
+    char* dst = nullptr;
+    size_t dpitch = 0, width = 0, rows = 0;
+  } out[kSlots];
+  int next = 0;
+  std::unique_ptr<CopyPool> pool;
+
+  void init() {  // on the owning device, lazily
+    if (pool) return;
+    for (int i = 0; i < kSlots; ++i) {
+      ck(cudaMallocHost(reinterpret_cast<void**>(&slot[i]), kSlotBytes), "cudaMallocHost(staging)");
+      ck(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    pool.reset(new CopyPool((int)std::min(8u, hw)));
+  }
+  void release() {
+    for (int i = 0; i < kSlots; ++i) {
+      if (slot[i]) cudaFreeHost(slot[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+      slot[i] = nullptr, ev[i] = nullptr;
+    }
+    pool.reset();
+  }
+  void reset() {  // a new call: forget copy-outs of an aborted one
+    for (auto& o : out) o.pending = false;
+  }
+  int acquire() {  // the oldest slot, once its DMA is done and its data copied out
+    const int i = next;
+    next = (next + 1) % kSlots;
+    ck(cudaEventSynchronize(ev[i]), "staging slot");
+    if (out[i].pending) {
+      copy_rows(*pool, out[i].dst, out[i].dpitch, slot[i], out[i].width, out[i].width, out[i].rows);
+      out[i].pending = false;
+    }
+    return i;
+  }
+  // host (pageable) -> device, pitched; enqueued on s
+  void h2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows, cudaStream_t s) {
+    if (!rows || !width) return;
+    if (width > kSlotBytes) {  // a row larger than a slot: the driver's path
+      ck(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyHostToDevice, s), "H2D");
+      return;
+    }
+    init();
+    const size_t per = kSlotBytes / width;
+    for (size_t r = 0; r < rows; r += per) {
+      const size_t pr = std::min(per, rows - r);
+      const int i = acquire();
+      copy_rows(*pool, slot[i], width, static_cast<const char*>(src) + r * spitch, spitch, width, pr);
+      ck(cudaMemcpy2DAsync(static_cast<char*>(dst) + r * dpitch, dpitch, slot[i], width, width, pr,
+                           cudaMemcpyHostToDevice, s),
+         "H2D (staged)");
+      ck(cudaEventRecord(ev[i], s), "event");
+    }
+  }
+  // device -> host (pageable), pitched; the copy-out happens when the slot
+  // is reused or at drain()
+  void d2h(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows, cudaStream_t s) {
+    if (!rows || !width) return;
+    if (width > kSlotBytes) {
+      ck(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, s), "D2H");
+      return;
+    }
+    init();
+    const size_t per = kSlotBytes / width;
+    for (size_t r = 0; r < rows; r += per) {
+      const size_t pr = std::min(per, rows - r);
+      const int i = acquire();
+      ck(cudaMemcpy2DAsync(slot[i], width, static_cast<const char*>(src) + r * spitch, spitch, width, pr,
+                           cudaMemcpyDeviceToHost, s),
+         "D2H (staged)");
+      ck(cudaEventRecord(ev[i], s), "event");
+      out[i] = Out{true, static_cast<char*>(dst) + r * dpitch, dpitch, width, pr};
+    }
+  }
+  void drain() {  // every pending copy-out, oldest first
+    for (int k = 0; k < kSlots; ++k) {
+      const int i = (next + k) % kSlots;
+      if (!out[i].pending) continue;
+      ck(cudaEventSynchronize(ev[i]), "staging slot");
+      copy_rows(*pool, out[i].dst, out[i].dpitch, slot[i], out[i].width, out[i].width, out[i].rows);
+      out[i].pending = false;
+    }
+  }
+};
+
 struct Device {
   int id = -1;
   bool ready = false;
@@ -118,6 +291,7 @@ struct Device {
   double* dB = nullptr;
   double* dC = nullptr;
   size_t capA = 0, capB = 0, capC = 0;
+  Stager stage;  // pageable host operands
 };
 
 std::mutex g_mu;
@@ -718,7 +892,56 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     const uint64_t pk = ((k + np - 1) / np + 15) / 16 * 16;  // even: 16-byte cp.async rows
     return {(int)((k + pk - 1) / pk), pk};
   };
+  // host<->device pitched copies: direct DMA for page-locked buffers, the
+  // device's pinned staging ring for pageable ones
+  const bool a_pin = !A->base || is_pinned(A->base);
+  const bool b_pin = !B->base || is_pinned(B->base);
+  const bool c_pin = !C->base || is_pinned(C->base);
+  auto copy_in = [&](Device& D, bool pinned, double* dst, uint64_t dld, const double* src, uint64_t sld,
+                 uint64_t cols, uint64_t nrows, cudaStream_t st) {
+    if (!cols || !nrows) return;
+    if (pinned)
+      ck(cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, cols * 8, nrows, cudaMemcpyHostToDevice, st), "H2D");
+    else
+      D.stage.h2d(dst, dld * 8, src, sld * 8, cols * 8, nrows, st);
+  };
+  auto copy_out = [&](Device& D, bool pinned, double* dst, uint64_t dld, const double* src, uint64_t sld,
+                 uint64_t cols, uint64_t nrows, cudaStream_t st) {
+    if (!cols || !nrows) return;
+    if (pinned)
+      ck(cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, cols * 8, nrows, cudaMemcpyDeviceToHost, st), "D2H");
+    else
+      D.stage.d2h(dst, dld * 8, src, sld * 8, cols * 8, nrows, st);
+  };
+  for (int g = 0; g < G; ++g) g_dev[sh[g].dev].stage.reset();
+
   std::vector<int> nchunks(G, 0);
+  auto upload_a = [&](int g, int c) {  // A row chunk c of shard g
+    Shard& s = sh[g];
+    Device& D = g_dev[s.dev];
+    const uint64_t rows = s.r1 - s.r0, crows = chunks_of(rows).second;
+    const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
+    for (int w = 0; w < W; ++w)
+      copy_in(D, a_pin, D.dA + w * rows * lda + c0 * lda, lda, A->base + w * pa_h + (s.r0 + c0) * A->stride,
+          A->stride, K, c1 - c0, D.up);
+    ck(cudaEventRecord(D.evA[c], D.up), "event");
+  };
+  // One GPU with pageable operands: the staged copies occupy the calling
+  // thread, so A chunks c >= 1 are staged just before chunk c's GEMM, and
+  // chunk 0's K-panel GEMMs are enqueued as each B panel lands, instead of
+  // after all uploads (with page-locked buffers the copies are asynchronous
+  // and the order of the calls does not matter).
+  const bool defer_a = G == 1 && !a_pin;
+  const bool panel_split0 = !(fast && splitk_plan(W, std::min<uint64_t>(m, chunks_of(m).second), n, K).S > 1);
+  const bool early0 = G == 1 && !b_pin && panels_of(K).first > 1 && panel_split0;
+  auto gemm_chunk0_panel = [&](Device& D, int p) {
+    const uint64_t rows = m, crows = chunks_of(rows).second, c1 = std::min<uint64_t>(rows, crows);
+    const uint64_t pk = panels_of(K).second, k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
+    if (p == 0) ck(cudaStreamWaitEvent(D.stream, D.evA[0], 0), "wait A chunk");
+    ck(cudaStreamWaitEvent(D.stream, D.evB[p], 0), "wait B panel");
+    return enqueue_gemm(W, c1, n, k1 - k0, D.dA + k0, lda, rows * lda, D.dB + k0 * ldb, ldb, K * ldb, D.dC, ldc,
+                        rows * ldc, D.stream, p > 0);
+  };
   auto phase1 = [&](int g) {  // allocate; upload A chunk 0, B (slice or K panels), other A chunks
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
@@ -727,42 +950,42 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(rows * lda, 1));
     grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
     grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(rows * ldc, 1));
-    const auto cpair = chunks_of(rows);
-    const uint64_t nc = cpair.first, crows = cpair.second;
-    nchunks[g] = rows ? (int)nc : 0;
-    auto upload_a = [&](int c) {
-      const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
-      for (int w = 0; w < W; ++w)
-        if (K)
-          ck(cudaMemcpy2DAsync(D.dA + w * rows * lda + c0 * lda, lda * 8,
-                               A->base + w * pa_h + (s.r0 + c0) * A->stride, A->stride * 8, K * 8,
-                               c1 - c0, cudaMemcpyHostToDevice, D.up),
-             "H2D A");
-      ck(cudaEventRecord(D.evA[c], D.up), "event");
-    };
+    nchunks[g] = rows ? (int)chunks_of(rows).first : 0;
     ck(cudaEventRecord(D.ev[0], D.up), "event");
-    if (nchunks[g]) upload_a(0);
+    if (early0) ck(cudaEventRecord(D.ev[2], D.stream), "event");
+    if (nchunks[g]) upload_a(g, 0);
     const auto ppair = panels_of(s.b1 - s.b0);
     const int np = ppair.first;
     const uint64_t pk = ppair.second;
     for (int p = 0; p < np; ++p) {
       const uint64_t k0 = s.b0 + p * pk, k1 = std::min<uint64_t>(s.b1, k0 + pk);
       for (int w = 0; w < W; ++w)
-        if (k1 > k0 && n)
-          ck(cudaMemcpy2DAsync(D.dB + w * K * ldb + k0 * ldb, ldb * 8, B->base + w * pb_h + k0 * B->stride,
-                               B->stride * 8, n * 8, k1 - k0, cudaMemcpyHostToDevice, D.up),
-             "H2D B");
+        if (k1 > k0)
+          copy_in(D, b_pin, D.dB + w * K * ldb + k0 * ldb, ldb, B->base + w * pb_h + k0 * B->stride, B->stride, n,
+              k1 - k0, D.up);
       ck(cudaEventRecord(D.evB[p], D.up), "event");
+      if (early0 && nchunks[g]) launches[g] += gemm_chunk0_panel(D, p);
     }
     ck(cudaEventRecord(D.ev[1], D.up), "event");
-    for (int c = 1; c < nchunks[g]; ++c) upload_a(c);
+    if (!defer_a)
+      for (int c = 1; c < nchunks[g]; ++c) upload_a(g, c);
+  };
+  auto download = [&](int g, int c) {  // C row chunk c of shard g, after its GEMM
+    Shard& s = sh[g];
+    Device& D = g_dev[s.dev];
+    const uint64_t rows = s.r1 - s.r0, crows = chunks_of(rows).second;
+    const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
+    ck(cudaStreamWaitEvent(D.down, D.evC[c], 0), "wait C chunk");
+    for (int w = 0; w < W; ++w)
+      copy_out(D, c_pin, C->base + w * pc_h + (s.r0 + c0) * C->stride, C->stride, D.dC + w * rows * ldc + c0 * ldc,
+               ldc, n, c1 - c0, D.down);
   };
   auto phase2 = [&](int g) {  // gather B slices from peers, compute chunks, download chunks
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
     ck(cudaSetDevice(D.id), "cudaSetDevice");
     const uint64_t rows = s.r1 - s.r0;
-    ck(cudaEventRecord(D.ev[2], D.stream), "event");
+    if (!early0) ck(cudaEventRecord(D.ev[2], D.stream), "event");
     if (peer) {
       ck(cudaStreamWaitEvent(D.stream, D.ev[1], 0), "wait B upload");
       for (int o = 0; o < G; ++o) {
@@ -785,8 +1008,11 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     for (int c = 0; c < nchunks[g]; ++c) {
       cudaStream_t cs = (c & 1) ? D.stream2 : D.stream;
       const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
+      if (defer_a && c > 0) upload_a(g, c);
       ck(cudaStreamWaitEvent(cs, D.evA[c], 0), "wait A chunk");
-      if (fast && splitk_plan(W, c1 - c0, n, K).S > 1) {
+      if (c == 0 && early0) {
+        // enqueued panel by panel in phase1
+      } else if (fast && splitk_plan(W, c1 - c0, n, K).S > 1) {
         ck(cudaStreamWaitEvent(cs, b_ready, 0), "wait B");
         launches[g] += enqueue_gemm_fast(W, c1 - c0, n, K, D.dA + c0 * lda, lda, rows * lda, D.dB, ldb,
                                          K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs);
@@ -804,19 +1030,19 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
                                     K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs);
       }
       ck(cudaEventRecord(D.evC[c], cs), "event");
-      ck(cudaStreamWaitEvent(D.down, D.evC[c], 0), "wait C chunk");
-      for (int w = 0; w < W; ++w)
-        ck(cudaMemcpy2DAsync(C->base + w * pc_h + (s.r0 + c0) * C->stride, C->stride * 8,
-                             D.dC + w * rows * ldc + c0 * ldc, ldc * 8, n * 8, c1 - c0,
-                             cudaMemcpyDeviceToHost, D.down),
-           "D2H C");
+      // pageable C: a staged download occupies this thread until its chunk
+      // is computed, so it trails by one chunk (GEMM c is already queued)
+      if (c_pin) download(g, c);
+      else if (c > 0) download(g, c - 1);
     }
+    if (!c_pin && nchunks[g]) download(g, nchunks[g] - 1);
     ck(cudaEventRecord(D.evJ, D.stream2), "event");
     ck(cudaStreamWaitEvent(D.stream, D.evJ, 0), "join");
     ck(cudaEventRecord(D.ev[3], D.stream), "event");
     ck(cudaStreamWaitEvent(D.down, D.ev[3], 0), "join");
     ck(cudaEventRecord(D.ev[4], D.down), "event");
     ck(cudaEventSynchronize(D.ev[4]), "GEMM execution");
+    D.stage.drain();
     const cudaEvent_t h2d_end = nchunks[g] > 1 ? D.evA[nchunks[g] - 1] : D.ev[1];
     cudaEventElapsedTime(&h2d[g], D.ev[0], h2d_end);
     bc[g] = 0.f;
@@ -1048,6 +1274,7 @@ void mpfk_shutdown(void) {
     cudaStreamDestroy(D.stream2);
     for (auto& e : D.evB) cudaEventDestroy(e);
     cudaEventDestroy(D.evJ);
+    D.stage.release();
     D = Device{};
   }
   g_dev.clear();

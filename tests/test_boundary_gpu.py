@@ -118,3 +118,24 @@ def test_set_device_mirrors_torch(gpu_lib):
     assert P.get_device() == 0
     with pytest.raises(ValueError, match="device index out of range"):
         P.set_device(P.device_count())
+
+
+@pytest.mark.parametrize("W,m,n,k", [(2, 2048, 5000, 64), (4, 700, 3000, 900)])
+def test_pageable_staging_multi_piece(gpu_lib, W, m, n, k):
+    """Pageable host operands go through libmpfk's pinned staging ring
+    (16 MiB slots, copy-outs deferred until a slot is reused): rows wider
+    than a slot's share, several pieces per plane and ring wrap-around must
+    give the same bits as page-locked operands and as the reference."""
+    P = gpu_lib
+    A = P.fill_baseline(W, m, k, 7, wide=True)
+    B = P.fill_baseline(W, k, n, 8, wide=True)
+    Cpage = P.MPMatrix(W, m, n)
+    Cpage.data[...] = 9.0
+    P.matmul_block_parallel_into(Cpage, A, B)
+    Ap, Bp = A.copy(pinned=True), B.copy(pinned=True)
+    Cpin = P.MPMatrix(W, m, n, pinned=True)
+    P.matmul_block_parallel_into(Cpin, Ap, Bp)
+    assert P.bits_equal(Cpage, Cpin)
+    rows = [0, m // 3, m - 1]
+    want = O.ref_gemm(np.ascontiguousarray(A.data[:, rows]), B.data, k, n)
+    assert mismatches(Cpage.data[:, rows], want) == 0
