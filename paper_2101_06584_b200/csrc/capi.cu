@@ -294,6 +294,26 @@ struct Device {
   Stager stage;  // pageable host operands
 };
 
+// host<->device pitched copies (strides in doubles): direct DMA for
+// page-locked host buffers, the device's staging ring for pageable ones
+void copy_h2d(Device& D, bool pinned, double* dst, uint64_t dld, const double* src, uint64_t sld, uint64_t cols,
+              uint64_t rows, cudaStream_t st) {
+  if (!cols || !rows) return;
+  if (pinned)
+    ck(cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, cols * 8, rows, cudaMemcpyHostToDevice, st), "H2D");
+  else
+    D.stage.h2d(dst, dld * 8, src, sld * 8, cols * 8, rows, st);
+}
+
+void copy_d2h(Device& D, bool pinned, double* dst, uint64_t dld, const double* src, uint64_t sld, uint64_t cols,
+              uint64_t rows, cudaStream_t st) {
+  if (!cols || !rows) return;
+  if (pinned)
+    ck(cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, cols * 8, rows, cudaMemcpyDeviceToHost, st), "D2H");
+  else
+    D.stage.d2h(dst, dld * 8, src, sld * 8, cols * 8, rows, st);
+}
+
 std::mutex g_mu;
 // Host-buffer calls share each device's grow-only operand buffers, streams
 // and events; they are serialised (each call is synchronous, like the
@@ -892,27 +912,9 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     const uint64_t pk = ((k + np - 1) / np + 15) / 16 * 16;  // even: 16-byte cp.async rows
     return {(int)((k + pk - 1) / pk), pk};
   };
-  // host<->device pitched copies: direct DMA for page-locked buffers, the
-  // device's pinned staging ring for pageable ones
   const bool a_pin = !A->base || is_pinned(A->base);
   const bool b_pin = !B->base || is_pinned(B->base);
   const bool c_pin = !C->base || is_pinned(C->base);
-  auto copy_in = [&](Device& D, bool pinned, double* dst, uint64_t dld, const double* src, uint64_t sld,
-                 uint64_t cols, uint64_t nrows, cudaStream_t st) {
-    if (!cols || !nrows) return;
-    if (pinned)
-      ck(cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, cols * 8, nrows, cudaMemcpyHostToDevice, st), "H2D");
-    else
-      D.stage.h2d(dst, dld * 8, src, sld * 8, cols * 8, nrows, st);
-  };
-  auto copy_out = [&](Device& D, bool pinned, double* dst, uint64_t dld, const double* src, uint64_t sld,
-                 uint64_t cols, uint64_t nrows, cudaStream_t st) {
-    if (!cols || !nrows) return;
-    if (pinned)
-      ck(cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, cols * 8, nrows, cudaMemcpyDeviceToHost, st), "D2H");
-    else
-      D.stage.d2h(dst, dld * 8, src, sld * 8, cols * 8, nrows, st);
-  };
   for (int g = 0; g < G; ++g) g_dev[sh[g].dev].stage.reset();
 
   std::vector<int> nchunks(G, 0);
@@ -922,7 +924,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     const uint64_t rows = s.r1 - s.r0, crows = chunks_of(rows).second;
     const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
     for (int w = 0; w < W; ++w)
-      copy_in(D, a_pin, D.dA + w * rows * lda + c0 * lda, lda, A->base + w * pa_h + (s.r0 + c0) * A->stride,
+      copy_h2d(D, a_pin, D.dA + w * rows * lda + c0 * lda, lda, A->base + w * pa_h + (s.r0 + c0) * A->stride,
           A->stride, K, c1 - c0, D.up);
     ck(cudaEventRecord(D.evA[c], D.up), "event");
   };
@@ -961,7 +963,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
       const uint64_t k0 = s.b0 + p * pk, k1 = std::min<uint64_t>(s.b1, k0 + pk);
       for (int w = 0; w < W; ++w)
         if (k1 > k0)
-          copy_in(D, b_pin, D.dB + w * K * ldb + k0 * ldb, ldb, B->base + w * pb_h + k0 * B->stride, B->stride, n,
+          copy_h2d(D, b_pin, D.dB + w * K * ldb + k0 * ldb, ldb, B->base + w * pb_h + k0 * B->stride, B->stride, n,
               k1 - k0, D.up);
       ck(cudaEventRecord(D.evB[p], D.up), "event");
       if (early0 && nchunks[g]) launches[g] += gemm_chunk0_panel(D, p);
@@ -977,7 +979,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
     ck(cudaStreamWaitEvent(D.down, D.evC[c], 0), "wait C chunk");
     for (int w = 0; w < W; ++w)
-      copy_out(D, c_pin, C->base + w * pc_h + (s.r0 + c0) * C->stride, C->stride, D.dC + w * rows * ldc + c0 * ldc,
+      copy_d2h(D, c_pin, C->base + w * pc_h + (s.r0 + c0) * C->stride, C->stride, D.dC + w * rows * ldc + c0 * ldc,
                ldc, n, c1 - c0, D.down);
   };
   auto phase2 = [&](int g) {  // gather B slices from peers, compute chunks, download chunks
@@ -1494,22 +1496,22 @@ int mpfk_ew_apply_into(int width, int op, mpfk_mat* out, const mpfk_mat* a, cons
       grow(D.dB, D.capB, sizeof(double) * width * ps);
       grow(D.dC, D.capC, sizeof(double) * width * ps);
       const uint64_t pa = plane_of(a), pb = plane_of(b), po = plane_of(out);
+      const bool a_pin = is_pinned(a->base), b_pin = is_pinned(b->base), o_pin = is_pinned(out->base);
+      D.stage.reset();
       ck(cudaEventRecord(D.ev[0], D.stream), "event");
       for (int w = 0; w < width; ++w) {
-        ck(cudaMemcpy2DAsync(D.dA + w * ps, ld * 8, a->base + w * pa, a->stride * 8, cols * 8, rows,
-                             cudaMemcpyHostToDevice, D.stream), "H2D a");
-        ck(cudaMemcpy2DAsync(D.dB + w * ps, ld * 8, b->base + w * pb, b->stride * 8, cols * 8, rows,
-                             cudaMemcpyHostToDevice, D.stream), "H2D b");
+        copy_h2d(D, a_pin, D.dA + w * ps, ld, a->base + w * pa, a->stride, cols, rows, D.stream);
+        copy_h2d(D, b_pin, D.dB + w * ps, ld, b->base + w * pb, b->stride, cols, rows, D.stream);
       }
       ck(cudaEventRecord(D.ev[1], D.stream), "event");
       st.kernel_launches = enqueue_ew(width, op, rows, cols, D.dC, ld, ps, D.dA, ld, ps, D.dB, ld, ps,
                                       D.stream);
       ck(cudaEventRecord(D.ev[2], D.stream), "event");
       for (int w = 0; w < width; ++w)
-        ck(cudaMemcpy2DAsync(out->base + w * po, out->stride * 8, D.dC + w * ps, ld * 8, cols * 8, rows,
-                             cudaMemcpyDeviceToHost, D.stream), "D2H out");
+        copy_d2h(D, o_pin, out->base + w * po, out->stride, D.dC + w * ps, ld, cols, rows, D.stream);
       ck(cudaEventRecord(D.ev[3], D.stream), "event");
       ck(cudaEventSynchronize(D.ev[3]), "ew execution");
+      D.stage.drain();
       float x = 0;
       cudaEventElapsedTime(&x, D.ev[0], D.ev[1]);
       st.h2d_ms = x;
