@@ -1906,7 +1906,8 @@ int mpfk_fp64_peak(double* ops_per_s, double* ms_out) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     double* d = nullptr;
     ck(cudaMalloc(&d, 8), "cudaMalloc");
-    const int blocks = sms * 8, threads = 256, iters = 4096;
+    // ~5 ms per launch so the launch ramp and tail are < 0.5 % of it
+    const int blocks = sms * 8, threads = 256, iters = 1 << 15;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
