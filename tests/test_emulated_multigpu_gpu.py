@@ -38,6 +38,17 @@ B = P.fill_baseline(2, 300, 70, 4, wide=True)
 G = P.gemm(A, B, n_gpus=0)
 out["gemm_all_devices"] = P.last_stats()["n_gpus"]
 out["gemm_same"] = P.bits_equal(G, P.matmul_block(A, B))
+# FAST across devices: shards too small to fill a GPU split K; the result is
+# deterministic and its leading components agree with the bit-exact product
+# within the north star's tolerance
+A = P.fill_baseline(3, 130, 4000, 5, wide=True)
+B = P.fill_baseline(3, 4000, 20, 6, wide=True)
+F1 = P.gemm(A, B, n_gpus=0, flags=P.FAST)
+F2 = P.gemm(A, B, n_gpus=0, flags=P.FAST)
+out["fast_deterministic"] = P.bits_equal(F1, F2)
+E = P.matmul_block(A, B)
+d = np.abs(F1.data[0] - E.data[0]).max()
+out["fast_close"] = bool(d <= 4 * 4000 * 2.0 ** -156 * np.abs(E.data[0]).max() + 1e-300)
 print(json.dumps(out))
 """
 
@@ -58,3 +69,4 @@ def test_multi_device_host_path_emulated(gpu_lib, emulated):
         assert (c["peer_bytes"] > 0) == (g > 1), c
     assert out["gemm_all_devices"] == emulated
     assert out["gemm_same"]
+    assert out["fast_deterministic"] and out["fast_close"]
