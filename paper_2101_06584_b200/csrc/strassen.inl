@@ -181,23 +181,23 @@ void host_strassen(int W, mpfk_mat* Cm, const mpfk_mat* A, const mpfk_mat* B, ui
   grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
   grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(m * ldc, 1));
   const uint64_t pa = plane_of(A), pb = plane_of(B), pc = plane_of(Cm);
+  const bool a_pin = !A->base || is_pinned(A->base), b_pin = !B->base || is_pinned(B->base);
+  const bool c_pin = is_pinned(Cm->base);
+  D.stage.reset();
   ck(cudaEventRecord(D.ev[0], D.stream), "event");
-  for (int w = 0; w < W; ++w)
-    if (K) {
-      ck(cudaMemcpy2DAsync(D.dA + w * m * lda, lda * 8, A->base + w * pa, A->stride * 8, K * 8, m,
-                           cudaMemcpyHostToDevice, D.stream), "H2D A");
-      ck(cudaMemcpy2DAsync(D.dB + w * K * ldb, ldb * 8, B->base + w * pb, B->stride * 8, n * 8, K,
-                           cudaMemcpyHostToDevice, D.stream), "H2D B");
-    }
+  for (int w = 0; w < W; ++w) {
+    copy_h2d(D, a_pin, D.dA + w * m * lda, lda, A->base + w * pa, A->stride, K, m, D.stream);
+    copy_h2d(D, b_pin, D.dB + w * K * ldb, ldb, B->base + w * pb, B->stride, n, K, D.stream);
+  }
   ck(cudaEventRecord(D.ev[1], D.stream), "event");
   st.kernel_launches = strassen_device(W, m, n, K, D.dA, lda, m * lda, D.dB, ldb, K * ldb, D.dC, ldc,
                                        m * ldc, cutoff, D.stream);
   ck(cudaEventRecord(D.ev[2], D.stream), "event");
   for (int w = 0; w < W; ++w)
-    ck(cudaMemcpy2DAsync(Cm->base + w * pc, Cm->stride * 8, D.dC + w * m * ldc, ldc * 8, n * 8, m,
-                         cudaMemcpyDeviceToHost, D.stream), "D2H C");
+    copy_d2h(D, c_pin, Cm->base + w * pc, Cm->stride, D.dC + w * m * ldc, ldc, n, m, D.stream);
   ck(cudaEventRecord(D.ev[3], D.stream), "event");
   ck(cudaEventSynchronize(D.ev[3]), "Strassen execution");
+  D.stage.drain();
   zero_host_pads(W, Cm);
   float x = 0;
   cudaEventElapsedTime(&x, D.ev[0], D.ev[1]);
