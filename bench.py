@@ -65,7 +65,10 @@ def parse():
                     help="initialise the NCCL process group and run the collective path even at N == 1")
     ap.add_argument("--fused-allgather", action="store_true",
                     help="B row-sliced across ranks and pulled over NVLink inside the GEMM kernel "
-                         "(mpfk_gemm_device_pull) instead of an NCCL broadcast")
+                         "(mpfk_gemm_device_pull) instead of an NCCL broadcast (the default at N > 1; "
+                         "this flag forces it at N == 1 with --dist)")
+    ap.add_argument("--nccl-bcast", action="store_true",
+                    help="N > 1: replicate B with NCCL broadcasts in K panels instead of the fused kernel")
     ap.add_argument("--pull-panel", type=int, default=256, help="fused all-gather: K rows per panel")
     ap.add_argument("--pull-chunk", type=int, default=16, help="fused all-gather: rows per copy chunk")
     ap.add_argument("--check", action="store_true",
@@ -270,13 +273,30 @@ def run_mpfk(args, ws, rank, local):
 
     overlap = use_dist and not args.no_overlap
     slices = None
-    if args.fused_allgather:
+    fused_note = None
+    # N > 1: the fused all-gather -> GEMM kernel (B pulled over NVLink peer
+    # memory inside the GEMM) unless --nccl-bcast; if the CUDA IPC mapping
+    # is unavailable on any rank, every rank falls back to the NCCL K-panel
+    # broadcast together
+    if args.fused_allgather or (ws > 1 and not args.nccl_bcast and not args.no_overlap):
         from paper_2101_06584_b200.dist import PeerBSlices
-        slices = PeerBSlices(W, k, ld)
-        c0, c1 = slices.cuts[slices.rank], slices.cuts[slices.rank + 1]
-        slices.upload(P.fill_baseline(W, c1 - c0, n, 2, wide=wide, row0=c0).data)
+        ok = 1
+        try:
+            slices = PeerBSlices(W, k, ld)
+            c0, c1 = slices.cuts[slices.rank], slices.cuts[slices.rank + 1]
+            slices.upload(P.fill_baseline(W, c1 - c0, n, 2, wide=wide, row0=c0).data)
+        except Exception as e:  # e.g. CUDA IPC not permitted in this container
+            ok = 0
+            fused_note = f"fused all-gather unavailable ({type(e).__name__}: {str(e)[:120]})"
+            print(f"bench: {fused_note}; using the NCCL K-panel broadcast", file=sys.stderr)
         if use_dist:
+            t = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            ok = int(t.item())
             dist.barrier()
+        if not ok and slices is not None:
+            slices.close()
+            slices = None
 
     def step():
         ev_mid = torch.cuda.Event(enable_timing=True)
@@ -414,6 +434,8 @@ def run_mpfk(args, ws, rank, local):
         achieved = rows * n * k * ops / (t_kern * 1e-3) / 1e9  # Gop/s
         traffic = load_traffic(args.workload) if ws == 1 else None  # captured on the 1-GPU launch
         parallelism = f"row-shard x{ws}"
+        if fused_note:
+            parallelism += f" [{fused_note}]"
         if slices is not None:
             parallelism += " + fused all-gather->GEMM (B pulled over peer memory inside the GEMM kernel)"
         elif overlap:

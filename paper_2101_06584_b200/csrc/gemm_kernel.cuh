@@ -174,8 +174,11 @@ __device__ __forceinline__ void pull_chunk(const PullB& P, const GemmArgs& g, in
 
 // Copy (without waiting) any still-unclaimed chunks of panel p: the
 // lookahead that lets CTAs entering panel p-1 stage panel p in advance.
+// (help_panel and ensure_panel are out of line: run once per panel, they
+// keep their registers out of the GEMM main loop, which then compiles to the
+// same instruction stream as the plain kernel's.)
 template <int W>
-__device__ void help_panel(const PullB& P, const GemmArgs& g, int p) {
+__device__ __noinline__ void help_panel(const PullB& P, const GemmArgs& g, int p) {
   __shared__ int s_ticket;
   if (p >= P.panels) return;
   for (;;) {
@@ -196,7 +199,7 @@ __device__ void help_panel(const PullB& P, const GemmArgs& g, int p) {
 
 // Make panel p of B resident (block-wide; see PullB).
 template <int W>
-__device__ void ensure_panel(const PullB& P, const GemmArgs& g, int p) {
+__device__ __noinline__ void ensure_panel(const PullB& P, const GemmArgs& g, int p) {
   __shared__ int s_state;
   if (threadIdx.x == 0) s_state = ld_acquire_gpu(&P.done[p]) >= P.chunks;
   __syncthreads();
