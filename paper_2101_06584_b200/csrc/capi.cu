@@ -201,7 +201,9 @@ struct Stager {
       ck(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "cudaEventCreate");
     }
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    pool.reset(new CopyPool((int)std::min(8u, hw)));
+    const char* env = std::getenv("MPFK_COPY_THREADS");
+    const int nthr = env && std::atoi(env) > 0 ? std::atoi(env) : (int)std::min(8u, hw);
+    pool.reset(new CopyPool(nthr));
   }
   void release() {
     for (int i = 0; i < kSlots; ++i) {
