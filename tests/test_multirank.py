@@ -181,25 +181,26 @@ def _worker_host(rank, world, port, W, m, k, n, panels, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("W,m,k,n,panels", [(2, 21, 50, 13, 3), (3, 9, 70, 5, 2), (4, 12, 33, 7, 8),
-                                            (2, 5, 31, 6, 1)])
-def test_two_rank_gloo_host_operands_sliced_b(W, m, k, n, panels):
-    """B starts on the host: each rank uploads 1/2 of every K panel, the
+@pytest.mark.parametrize("world,W,m,k,n,panels", [(2, 2, 21, 50, 13, 3), (2, 3, 9, 70, 5, 2), (2, 4, 12, 33, 7, 8),
+                                                  (2, 2, 5, 31, 6, 1), (3, 2, 30, 61, 9, 2), (3, 4, 7, 40, 5, 3)])
+def test_gloo_host_operands_sliced_b(world, W, m, k, n, panels):
+    """B starts on the host: each rank uploads 1/world of every K panel, the
     panels are all-gathered, the shard GEMM continues panel by panel; the
     assembled C is bit-identical to the one-shot product, including ragged
-    last panels (k not a multiple of the panel height)."""
+    last panels (k not a multiple of the panel height) and ranks without
+    rows."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_host, args=(r, 2, port, W, m, k, n, panels, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker_host, args=(r, world, port, W, m, k, n, panels, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(120)
+        p.join(180)
     assert all(p.exitcode == 0 for p in procs)
     same, launches = q.get(timeout=10)
     from paper_2101_06584_b200.dist import gather_panels
-    assert same and launches == len(gather_panels(k, panels, 2)[1])
+    assert same and launches == len(gather_panels(k, panels, world)[1])
 
 
 def test_gather_panels_plan():
