@@ -9,6 +9,7 @@
 //   run_on_threads (linalg.hpp:314-334) -> one host thread per GPU
 //   count_matmul / op counters (linalg.hpp:160-180, linalg.cpp:10-25)
 //   rng + fill generators (random.hpp)
+#include <cuda.h>  // driver types only: entry points are resolved at run time
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -293,6 +294,8 @@ struct Device {
   double* dB = nullptr;
   double* dC = nullptr;
   size_t capA = 0, capB = 0, capC = 0;
+  unsigned* gate = nullptr;  // gated path: K-panel flags + row-band tile counters
+  size_t gate_cap = 0;
   Stager stage;  // pageable host operands
 };
 
@@ -623,6 +626,70 @@ int dispatch_gemm_splitk(int W, const kern::GemmArgs& g, int klast, cudaStream_t
   return 1;
 }
 
+// ---------------------------------------------------------------------------
+// copy-engine-gated GEMM (host operands streamed in K panels)
+// ---------------------------------------------------------------------------
+// Stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32) are
+// driver API; their entry points are resolved through the runtime so the
+// library does not link libcuda.  Unavailable -> the chunked host path.
+using MemOpFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+MemOpFn g_write32 = nullptr, g_wait32 = nullptr;
+std::once_flag g_memops_once;
+
+bool memops_available() {
+  std::call_once(g_memops_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &f, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_write32 = reinterpret_cast<MemOpFn>(f);
+    f = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &f, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_wait32 = reinterpret_cast<MemOpFn>(f);
+    cudaGetLastError();
+    if (const char* e = std::getenv("MPFK_NO_GATED"); e && std::atoi(e) > 0) g_write32 = g_wait32 = nullptr;
+  });
+  return g_write32 && g_wait32;
+}
+
+void cu_ck(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) fail(MPFK_ECUDA, std::string("mpfk: ") + what + " failed (CUresult " + std::to_string(r) + ")");
+}
+
+template <class Cfg>
+std::pair<int, int> launch_gated_cfg(const kern::GemmArgs& g, const kern::GateArgs& G, cudaStream_t s) {
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    ck(cudaFuncSetAttribute(kern::mpgemm_gated_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)Cfg::SMEM),
+       "cudaFuncSetAttribute");
+    configured_dev = dev;
+  }
+  if (G.panel_rows % Cfg::BK || G.band_rows % Cfg::BM) fail(MPFK_EINVAL, "mpfk: gated panel/band size");
+  const long long tiles = tiles_of<Cfg>(g);
+  if (tiles > 0x7fffffffLL) fail(MPFK_EINVAL, "mpfk: too many tiles");
+  kern::mpgemm_gated_kernel<Cfg><<<(unsigned)tiles, Cfg::THREADS, Cfg::SMEM, s>>>(g, G);
+  ck(cudaGetLastError(), "gated GEMM launch");
+  return {Cfg::BM, Cfg::BN};
+}
+
+// the same configuration choice as dispatch_gemm; returns the tile (BM, BN)
+std::pair<int, int> dispatch_gemm_gated(int W, const kern::GemmArgs& g, const kern::GateArgs& G, cudaStream_t s) {
+  switch (W) {
+    case 2:
+      if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944)) return launch_gated_cfg<Cfg2s>(g, G, s);
+      return launch_gated_cfg<Cfg2>(g, G, s);
+    case 3: return launch_gated_cfg<Cfg3>(g, G, s);
+    case 4: return launch_gated_cfg<Cfg4>(g, G, s);
+    default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
+  }
+}
+
 int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s) {
   switch (W) {
     case 2:
@@ -798,6 +865,128 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// The gated single launch stalls while its first wave of tiles consumes K
+// panels faster than PCIe delivers them; it pays when the whole upload fits
+// in about two first-wave durations (measured: DD/TD/QD n=1024, TD/QD n=4096
+// gain; DD n=8192 -- 2 GiB of operands against an 11 ms first wave -- keeps
+// the row-chunked path, whose chunk-0 GEMM walks B panel by panel).
+bool gate_pays(int W, uint64_t m, uint64_t n, uint64_t K) {
+  kern::GemmArgs g;
+  g.M = (int)std::min<uint64_t>(m, 0x7fffffff), g.N = (int)std::min<uint64_t>(n, 0x7fffffff), g.batch = 1;
+  int BM = Cfg3::BM, BN = Cfg3::BN, minb = Cfg3::MINB;
+  if (W == 4) BM = Cfg4::BM, BN = Cfg4::BN, minb = Cfg4::MINB;
+  if (W == 2) {
+    if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
+      BM = Cfg2s::BM, BN = Cfg2s::BN, minb = Cfg2s::MINB;
+    else
+      BM = Cfg2::BM, BN = Cfg2::BN, minb = Cfg2::MINB;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const double tiles = double((m + BM - 1) / BM) * double((n + BN - 1) / BN);
+  const double waves = std::max(1.0, tiles / (double(sms) * minb));
+  const double ops = W == 2 ? 20.0 : W == 3 ? 132.0 : 218.0;
+  const double kern_s = double(m) * n * K * ops / 18e12;                   // ~FP64 peak
+  const double upload_s = 8.0 * W * (double(m) * K + double(K) * n) / 50e9;  // ~PCIe 5 x16
+  return upload_s <= 2.0 * kern_s / waves;
+}
+
+// One GPU, page-locked host operands: ONE GEMM launch gated by the copy
+// engines.  A and B are uploaded in K panels on the copy stream, each
+// followed by a stream memory write of the panel's flag; the kernel waits on
+// a panel's flag before staging its first k-tile (kern::GateArgs), so it
+// starts once the first panel has landed and never waits again while the
+// copies stay ahead.  Finished tiles count per 256-row band; the download
+// stream waits on each band's count (stream wait-value) and copies it out
+// while later bands compute.  No chunking: the kernel keeps its full-size
+// tile grid (the chunked path's under-filled launches were the main loss on
+// small shapes).
+void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, Device& D, mpfk_stats& st) {
+  const uint64_t m = A->rows, K = A->cols, n = B->cols;
+  const uint64_t lda = pad4(K), ldb = pad4(n), ldc = pad4(n);
+  const uint64_t pa_h = plane_of(A), pb_h = plane_of(B), pc_h = plane_of(C);
+  ck(cudaSetDevice(D.id), "cudaSetDevice");
+  grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(m * lda, 1));
+  grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
+  grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(m * ldc, 1));
+  // K panels: >= 256 k steps, at most 32, a multiple of BK = 16 rows each
+  const uint64_t np0 = std::max<uint64_t>(1, std::min<uint64_t>(32, K / 256));
+  const uint64_t pk = ((K + np0 - 1) / np0 + 15) / 16 * 16;
+  const uint64_t npan = (K + pk - 1) / pk;
+  const uint64_t band_rows = 256;  // a multiple of every configuration's BM
+  const uint64_t nb = (m + band_rows - 1) / band_rows;
+  const size_t gate_bytes = sizeof(unsigned) * (npan + nb);
+  if (gate_bytes > D.gate_cap) {
+    if (D.gate) cudaFree(D.gate);
+    D.gate = nullptr;
+    D.gate_cap = 0;
+    ck(cudaMalloc(reinterpret_cast<void**>(&D.gate), gate_bytes), "cudaMalloc(gate)");
+    D.gate_cap = gate_bytes;
+  }
+  unsigned* flags = D.gate;
+  unsigned* band_done = D.gate + npan;
+
+  ck(cudaEventRecord(D.ev[0], D.up), "event");
+  ck(cudaMemsetAsync(D.gate, 0, gate_bytes, D.up), "cudaMemsetAsync(gate)");
+  ck(cudaEventRecord(D.ev[5], D.up), "event");  // flags and counters cleared
+  for (uint64_t p = 0; p < npan; ++p) {
+    const uint64_t k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
+    for (int w = 0; w < W; ++w) {
+      ck(cudaMemcpy2DAsync(D.dA + w * m * lda + k0, lda * 8, A->base + w * pa_h + k0, A->stride * 8,
+                           (k1 - k0) * 8, m, cudaMemcpyHostToDevice, D.up),
+         "H2D A panel");
+      ck(cudaMemcpy2DAsync(D.dB + w * K * ldb + k0 * ldb, ldb * 8, B->base + w * pb_h + k0 * B->stride,
+                           B->stride * 8, n * 8, k1 - k0, cudaMemcpyHostToDevice, D.up),
+         "H2D B panel");
+    }
+    cu_ck(g_write32(reinterpret_cast<CUstream>(D.up), reinterpret_cast<CUdeviceptr>(flags + p), 1, 0),
+          "cuStreamWriteValue32");
+  }
+  ck(cudaEventRecord(D.ev[1], D.up), "event");
+
+  ck(cudaStreamWaitEvent(D.stream, D.ev[5], 0), "wait gate reset");
+  ck(cudaEventRecord(D.ev[2], D.stream), "event");
+  kern::GemmArgs g;
+  g.A = D.dA, g.B = D.dB, g.C = D.dC;
+  g.lda = (long long)lda, g.ldb = (long long)ldb, g.ldc = (long long)ldc;
+  g.pa = (long long)(m * lda), g.pb = (long long)(K * ldb), g.pc = (long long)(m * ldc);
+  g.M = (int)m, g.N = (int)n, g.K = (int)K;
+  g.accumulate = 0;
+  g.batch = 1, g.sa = g.sb = g.sc = 0;
+  kern::GateArgs gate{flags, band_done, (int)pk, (int)band_rows};
+  const auto tile = dispatch_gemm_gated(W, g, gate, D.stream);
+  ck(cudaEventRecord(D.ev[3], D.stream), "event");
+
+  ck(cudaStreamWaitEvent(D.down, D.ev[5], 0), "wait gate reset");
+  const uint64_t tiles_n = (n + tile.second - 1) / tile.second;
+  for (uint64_t b = 0; b < nb; ++b) {
+    const uint64_t r0 = b * band_rows, r1 = std::min<uint64_t>(m, r0 + band_rows);
+    const uint64_t tiles = (r1 - r0 + tile.first - 1) / tile.first * tiles_n;
+    cu_ck(g_wait32(reinterpret_cast<CUstream>(D.down), reinterpret_cast<CUdeviceptr>(band_done + b),
+                   (cuuint32_t)tiles, CU_STREAM_WAIT_VALUE_GEQ),
+          "cuStreamWaitValue32");
+    for (int w = 0; w < W; ++w)
+      ck(cudaMemcpy2DAsync(C->base + w * pc_h + r0 * C->stride, C->stride * 8, D.dC + w * m * ldc + r0 * ldc,
+                           ldc * 8, n * 8, r1 - r0, cudaMemcpyDeviceToHost, D.down),
+         "D2H C band");
+  }
+  ck(cudaStreamWaitEvent(D.down, D.ev[3], 0), "join");
+  ck(cudaEventRecord(D.ev[4], D.down), "event");
+  ck(cudaEventSynchronize(D.ev[4]), "GEMM execution");
+  float x = 0;
+  cudaEventElapsedTime(&x, D.ev[0], D.ev[1]);
+  st.h2d_ms = x;
+  cudaEventElapsedTime(&x, D.ev[2], D.ev[3]);
+  st.kernel_ms = x;
+  cudaEventElapsedTime(&x, D.ev[3], D.ev[4]);
+  st.d2h_ms = x;
+  st.h2d_bytes = 8ull * W * (m * K + K * n);
+  st.d2h_bytes = 8ull * W * m * n;
+  st.kernel_launches = 1;
+  st.n_gpus = 1;
+}
+
 // One GPU's share of a host-buffer GEMM: rows [r0, r1) of C.
 struct Shard {
   int dev;
@@ -917,6 +1106,18 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   const bool a_pin = !A->base || is_pinned(A->base);
   const bool b_pin = !B->base || is_pinned(B->base);
   const bool c_pin = !C->base || is_pinned(C->base);
+  if (G == 1 && a_pin && b_pin && c_pin && K > 0 && !std::getenv("MPFK_CHUNKED_HOST") && gate_pays(W, m, n, K) &&
+      memops_available() && !(fast && splitk_plan(W, m, n, K).S > 1)) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    host_gemm_gated(W, C, A, B, g_dev[sh[0].dev], st);
+    cudaSetDevice(prev);
+    zero_host_pads(W, C);
+    count_matmul(m, n, K);
+    st.total_ms = ms_since(t0);
+    t_stats = st;
+    return;
+  }
   for (int g = 0; g < G; ++g) g_dev[sh[g].dev].stage.reset();
 
   std::vector<int> nchunks(G, 0);
@@ -1269,6 +1470,7 @@ void mpfk_shutdown(void) {
     if (D.dA) cudaFree(D.dA);
     if (D.dB) cudaFree(D.dB);
     if (D.dC) cudaFree(D.dC);
+    if (D.gate) cudaFree(D.gate);
     for (auto& e : D.ev) cudaEventDestroy(e);
     for (auto& e : D.evA) cudaEventDestroy(e);
     for (auto& e : D.evC) cudaEventDestroy(e);

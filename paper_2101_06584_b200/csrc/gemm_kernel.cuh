@@ -227,6 +227,31 @@ __device__ __noinline__ void ensure_panel(const PullB& P, const GemmArgs& g, int
   __syncthreads();
 }
 
+// Copy-engine-gated GEMM (host operands streamed in K panels, see
+// capi.cu:host_gemm_gated): panel p of A and B is resident once flags[p] is
+// nonzero -- written by the copy stream with a stream memory operation after
+// the panel's copies, so no SM time goes into the transfer -- and each
+// finished tile adds 1 to band_done[m0 / band_rows], which the download
+// stream waits on (stream wait-value) before copying that row band of C.
+struct GateArgs {
+  const unsigned* flags;
+  unsigned* band_done;
+  int panel_rows;  // multiple of BK
+  int band_rows;   // multiple of BM
+};
+
+// out of line: the main loop keeps the plain kernel's code generation
+__device__ __noinline__ void wait_flag(const unsigned* f) {
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    while (ld_acquire_gpu(reinterpret_cast<const int*>(f)) == 0) {
+      __nanosleep(256);
+      if (clock64() - t0 > (1ll << 37)) __trap();  // ~70 s without the copy: fail loudly
+    }
+  }
+  __syncthreads();
+}
+
 // one k step of the register micro-tile: C (+)= A(:, kk) * B(kk, :)
 template <class Cfg>
 __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W], const double* As,
@@ -252,8 +277,11 @@ __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W]
     }
 }
 
-template <class Cfg, bool kPull>
-__device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, int klast = 0) {
+// kMode: 0 plain, 1 fused all-gather (PullB), 2 copy-engine gated (GateArgs)
+template <class Cfg, int kMode>
+__device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, int klast = 0,
+                                          const GateArgs& G = GateArgs{}) {
+  constexpr bool kPull = kMode == 1, kGate = kMode == 2;
   constexpr int W = Cfg::W, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, TX = Cfg::TX, TY = Cfg::TY;
   constexpr int STAGES = Cfg::STAGES;
@@ -302,6 +330,10 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, in
         ensure_panel<W>(P, g, ready_panel);
         help_panel<W>(P, g, ready_panel + 1);
       }
+      if (kGate && s * BK / G.panel_rows > ready_panel) {
+        ready_panel = s * BK / G.panel_rows;
+        wait_flag(G.flags + ready_panel);
+      }
       load_tile<Cfg>(As0 + s * Cfg::A_STAGE, Bs0 + s * Cfg::B_STAGE, g, m0, n0, s * BK);
     }
     cp_async_commit();
@@ -317,6 +349,10 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, in
           ready_panel = nt * BK / P.panel_rows;
           ensure_panel<W>(P, g, ready_panel);
           help_panel<W>(P, g, ready_panel + 1);
+        }
+        if (kGate && nt * BK / G.panel_rows > ready_panel) {
+          ready_panel = nt * BK / G.panel_rows;
+          wait_flag(G.flags + ready_panel);
         }
         load_tile<Cfg>(As0 + slot * Cfg::A_STAGE, Bs0 + slot * Cfg::B_STAGE, g, m0, n0, nt * BK);
       }
@@ -371,11 +407,18 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, in
       for (int w = 0; w < W; ++w) g.C[w * g.pc + (long long)gm * g.ldc + gn] = acc[i][j][w];
     }
   }
+  if (kGate) {  // publish the finished tile to the download stream
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(G.band_done + m0 / G.band_rows, 1u);
+    }
+  }
 }
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_kernel(const GemmArgs g0) {
-  gemm_body<Cfg, false>(g0, PullB{});
+  gemm_body<Cfg, 0>(g0, PullB{});
 }
 
 // MPFK_FAST split-K (csrc/splitk.cuh): the batch is the K segments, the
@@ -383,13 +426,20 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_kernel(const G
 // kernels keep their code generation).
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_splitk_kernel(const GemmArgs g0, int klast) {
-  gemm_body<Cfg, false>(g0, PullB{}, klast);
+  gemm_body<Cfg, 0>(g0, PullB{}, klast);
 }
 
 // The fused all-gather -> GEMM (see PullB); batch must be 1.
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_pull_kernel(const GemmArgs g0, const PullB pull) {
-  gemm_body<Cfg, true>(g0, pull);
+  gemm_body<Cfg, 1>(g0, pull);
+}
+
+// Host operands streamed by the copy engines in K panels (see GateArgs);
+// batch must be 1.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_gated_kernel(const GemmArgs g0, const GateArgs gate) {
+  gemm_body<Cfg, 2>(g0, PullB{}, 0, gate);
 }
 
 }  // namespace kern

@@ -139,3 +139,26 @@ def test_pageable_staging_multi_piece(gpu_lib, W, m, n, k):
     rows = [0, m // 3, m - 1]
     want = O.ref_gemm(np.ascontiguousarray(A.data[:, rows]), B.data, k, n)
     assert mismatches(Cpage.data[:, rows], want) == 0
+
+
+@pytest.mark.parametrize("W,m,n,k", [(2, 700, 300, 1100), (3, 257, 129, 2000), (4, 100, 40, 5000),
+                                     (2, 33, 7, 17), (3, 1, 1, 600)])
+def test_gated_host_path_bitwise(gpu_lib, W, m, n, k, monkeypatch):
+    """Page-locked host operands on one GPU take the copy-engine-gated single
+    launch when it pays (K panels flagged by stream memory writes, row bands
+    downloaded on stream wait-values); it must give the reference's bits and
+    the same bits as the row-chunked path (MPFK_CHUNKED_HOST=1)."""
+    P = gpu_lib
+    A = P.fill_baseline(W, m, k, 11, wide=True, pinned=True)
+    B = P.fill_baseline(W, k, n, 12, wide=True, pinned=True)
+    Cg = P.MPMatrix(W, m, n, pinned=True)
+    Cg.data[...] = 5.0
+    P.matmul_block_parallel_into(Cg, A, B)
+    gated = P.last_stats()["kernel_launches"] == 1
+    monkeypatch.setenv("MPFK_CHUNKED_HOST", "1")
+    Cc = P.MPMatrix(W, m, n, pinned=True)
+    P.matmul_block_parallel_into(Cc, A, B)
+    assert P.bits_equal(Cg, Cc)
+    want = O.ref_gemm(A.data, B.data, k, n)
+    assert mismatches(Cg.data, want) == 0
+    assert gated or k < 256  # these shapes are small enough for the gated path
