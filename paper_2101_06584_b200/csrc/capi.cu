@@ -651,6 +651,23 @@ bool memops_available() {
       g_wait32 = reinterpret_cast<MemOpFn>(f);
     cudaGetLastError();
     if (const char* e = std::getenv("MPFK_NO_GATED"); e && std::atoi(e) > 0) g_write32 = g_wait32 = nullptr;
+    if (!g_write32 || !g_wait32) return;
+    // probe once on the current device: write a value, wait for it, read it back
+    unsigned* d = nullptr;
+    cudaStream_t st = nullptr;
+    unsigned h = 0;
+    bool ok = cudaMalloc(reinterpret_cast<void**>(&d), sizeof(unsigned)) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMemsetAsync(d, 0, sizeof(unsigned), st) == cudaSuccess &&
+              g_write32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(d), 7, 0) == CUDA_SUCCESS &&
+              g_wait32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(d), 7,
+                       CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS &&
+              cudaMemcpyAsync(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+              cudaStreamSynchronize(st) == cudaSuccess && h == 7;
+    if (st) cudaStreamDestroy(st);
+    if (d) cudaFree(d);
+    cudaGetLastError();
+    if (!ok) g_write32 = g_wait32 = nullptr;
   });
   return g_write32 && g_wait32;
 }
