@@ -887,7 +887,7 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
 // in about two first-wave durations (measured: DD/TD/QD n=1024, TD/QD n=4096
 // gain; DD n=8192 -- 2 GiB of operands against an 11 ms first wave -- keeps
 // the row-chunked path, whose chunk-0 GEMM walks B panel by panel).
-bool gate_pays(int W, uint64_t m, uint64_t n, uint64_t K) {
+bool gate_pays(int W, uint64_t m, uint64_t n, uint64_t K, double upload_bw) {
   kern::GemmArgs g;
   g.M = (int)std::min<uint64_t>(m, 0x7fffffff), g.N = (int)std::min<uint64_t>(n, 0x7fffffff), g.batch = 1;
   int BM = Cfg3::BM, BN = Cfg3::BN, minb = Cfg3::MINB;
@@ -905,13 +905,14 @@ bool gate_pays(int W, uint64_t m, uint64_t n, uint64_t K) {
   const double waves = std::max(1.0, tiles / (double(sms) * minb));
   const double ops = W == 2 ? 20.0 : W == 3 ? 132.0 : 218.0;
   const double kern_s = double(m) * n * K * ops / 18e12;                   // ~FP64 peak
-  const double upload_s = 8.0 * W * (double(m) * K + double(K) * n) / 50e9;  // ~PCIe 5 x16
+  const double upload_s = 8.0 * W * (double(m) * K + double(K) * n) / upload_bw;
   return upload_s <= 2.0 * kern_s / waves;
 }
 
-// One GPU, page-locked host operands: ONE GEMM launch gated by the copy
-// engines.  A and B are uploaded in K panels on the copy stream, each
-// followed by a stream memory write of the panel's flag; the kernel waits on
+// One GPU: ONE GEMM launch gated by the copy engines.  A and B are uploaded
+// in K panels on the copy stream (directly, or through the staging ring for
+// pageable operands), each followed by a stream memory write of the panel's
+// flag; the kernel, enqueued before the uploads, waits on
 // a panel's flag before staging its first k-tile (kern::GateArgs), so it
 // starts once the first panel has landed and never waits again while the
 // copies stay ahead.  Finished tiles count per 256-row band; the download
@@ -919,7 +920,8 @@ bool gate_pays(int W, uint64_t m, uint64_t n, uint64_t K) {
 // while later bands compute.  No chunking: the kernel keeps its full-size
 // tile grid (the chunked path's under-filled launches were the main loss on
 // small shapes).
-void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, Device& D, mpfk_stats& st) {
+void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, Device& D, mpfk_stats& st,
+                     bool a_pin, bool b_pin, bool c_pin) {
   const uint64_t m = A->rows, K = A->cols, n = B->cols;
   const uint64_t lda = pad4(K), ldb = pad4(n), ldc = pad4(n);
   const uint64_t pa_h = plane_of(A), pb_h = plane_of(B), pc_h = plane_of(C);
@@ -944,24 +946,14 @@ void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, D
   unsigned* flags = D.gate;
   unsigned* band_done = D.gate + npan;
 
+  D.stage.reset();
   ck(cudaEventRecord(D.ev[0], D.up), "event");
   ck(cudaMemsetAsync(D.gate, 0, gate_bytes, D.up), "cudaMemsetAsync(gate)");
   ck(cudaEventRecord(D.ev[5], D.up), "event");  // flags and counters cleared
-  for (uint64_t p = 0; p < npan; ++p) {
-    const uint64_t k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
-    for (int w = 0; w < W; ++w) {
-      ck(cudaMemcpy2DAsync(D.dA + w * m * lda + k0, lda * 8, A->base + w * pa_h + k0, A->stride * 8,
-                           (k1 - k0) * 8, m, cudaMemcpyHostToDevice, D.up),
-         "H2D A panel");
-      ck(cudaMemcpy2DAsync(D.dB + w * K * ldb + k0 * ldb, ldb * 8, B->base + w * pb_h + k0 * B->stride,
-                           B->stride * 8, n * 8, k1 - k0, cudaMemcpyHostToDevice, D.up),
-         "H2D B panel");
-    }
-    cu_ck(g_write32(reinterpret_cast<CUstream>(D.up), reinterpret_cast<CUdeviceptr>(flags + p), 1, 0),
-          "cuStreamWriteValue32");
-  }
-  ck(cudaEventRecord(D.ev[1], D.up), "event");
 
+  // the kernel is enqueued first: it starts computing as soon as panel 0's
+  // flag is written, while this thread is still issuing (or, for pageable
+  // operands, staging) the later panels
   ck(cudaStreamWaitEvent(D.stream, D.ev[5], 0), "wait gate reset");
   ck(cudaEventRecord(D.ev[2], D.stream), "event");
   kern::GemmArgs g;
@@ -975,6 +967,18 @@ void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, D
   const auto tile = dispatch_gemm_gated(W, g, gate, D.stream);
   ck(cudaEventRecord(D.ev[3], D.stream), "event");
 
+  for (uint64_t p = 0; p < npan; ++p) {
+    const uint64_t k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
+    for (int w = 0; w < W; ++w) {
+      copy_h2d(D, a_pin, D.dA + w * m * lda + k0, lda, A->base + w * pa_h + k0, A->stride, k1 - k0, m, D.up);
+      copy_h2d(D, b_pin, D.dB + w * K * ldb + k0 * ldb, ldb, B->base + w * pb_h + k0 * B->stride, B->stride, n,
+               k1 - k0, D.up);
+    }
+    cu_ck(g_write32(reinterpret_cast<CUstream>(D.up), reinterpret_cast<CUdeviceptr>(flags + p), 1, 0),
+          "cuStreamWriteValue32");
+  }
+  ck(cudaEventRecord(D.ev[1], D.up), "event");
+
   ck(cudaStreamWaitEvent(D.down, D.ev[5], 0), "wait gate reset");
   const uint64_t tiles_n = (n + tile.second - 1) / tile.second;
   for (uint64_t b = 0; b < nb; ++b) {
@@ -984,13 +988,13 @@ void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, D
                    (cuuint32_t)tiles, CU_STREAM_WAIT_VALUE_GEQ),
           "cuStreamWaitValue32");
     for (int w = 0; w < W; ++w)
-      ck(cudaMemcpy2DAsync(C->base + w * pc_h + r0 * C->stride, C->stride * 8, D.dC + w * m * ldc + r0 * ldc,
-                           ldc * 8, n * 8, r1 - r0, cudaMemcpyDeviceToHost, D.down),
-         "D2H C band");
+      copy_d2h(D, c_pin, C->base + w * pc_h + r0 * C->stride, C->stride, D.dC + w * m * ldc + r0 * ldc, ldc, n,
+               r1 - r0, D.down);
   }
   ck(cudaStreamWaitEvent(D.down, D.ev[3], 0), "join");
   ck(cudaEventRecord(D.ev[4], D.down), "event");
   ck(cudaEventSynchronize(D.ev[4]), "GEMM execution");
+  D.stage.drain();
   float x = 0;
   cudaEventElapsedTime(&x, D.ev[0], D.ev[1]);
   st.h2d_ms = x;
@@ -1123,11 +1127,14 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   const bool a_pin = !A->base || is_pinned(A->base);
   const bool b_pin = !B->base || is_pinned(B->base);
   const bool c_pin = !C->base || is_pinned(C->base);
-  if (G == 1 && a_pin && b_pin && c_pin && K > 0 && !std::getenv("MPFK_CHUNKED_HOST") && gate_pays(W, m, n, K) &&
-      memops_available() && !(fast && splitk_plan(W, m, n, K).S > 1)) {
+  // (pageable operands keep the chunked path: measured, staging A's narrow
+  // K-panel columns through the copy threads costs more than the single
+  // launch saves)
+  if (G == 1 && a_pin && b_pin && c_pin && K > 0 && !std::getenv("MPFK_CHUNKED_HOST") &&
+      gate_pays(W, m, n, K, 50e9) && memops_available() && !(fast && splitk_plan(W, m, n, K).S > 1)) {
     int prev = 0;
     cudaGetDevice(&prev);
-    host_gemm_gated(W, C, A, B, g_dev[sh[0].dev], st);
+    host_gemm_gated(W, C, A, B, g_dev[sh[0].dev], st, a_pin, b_pin, c_pin);
     cudaSetDevice(prev);
     zero_host_pads(W, C);
     count_matmul(m, n, K);
