@@ -70,7 +70,8 @@ def parse():
     ap.add_argument("--nccl-bcast", action="store_true",
                     help="N > 1: replicate B with NCCL broadcasts in K panels instead of the fused kernel")
     ap.add_argument("--pull-panel", type=int, default=256, help="fused all-gather: K rows per panel")
-    ap.add_argument("--pull-chunk", type=int, default=16, help="fused all-gather: rows per copy chunk")
+    ap.add_argument("--pull-chunk", type=int, default=2,
+                    help="fused all-gather: rows per copy chunk (small chunks spread each panel over many CTAs)")
     ap.add_argument("--check", action="store_true",
                     help="after timing, check the sharded step's C bitwise against a plain one-shot GEMM")
     return ap.parse_args()

@@ -291,7 +291,7 @@ class PeerBSlices:
         if a.size:
             L.memcpy(self.local, a.ctypes.data, a.nbytes)
 
-    def step(self, W, dA, dB, dC, rows, n, k, panel_rows=256, chunk_rows=16, stream=None) -> int:
+    def step(self, W, dA, dB, dC, rows, n, k, panel_rows=256, chunk_rows=2, stream=None) -> int:
         """C_shard = A_shard * B with B pulled from the slices inside the GEMM."""
         from . import linalg as L
         if rows == 0:
