@@ -67,15 +67,18 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>}
 
 const Entry kEntries[] = {
-    E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // product, large
-    E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // product, few waves
-    E(2, 32, 32, 16, 4, 4, 2, 2, 16, 6),  // 64 threads
-    E(2, 32, 32, 8, 4, 4, 2, 2, 16, 8),
-    E(2, 32, 32, 16, 4, 4, 2, 2, 16, 4),
-    E(2, 64, 32, 16, 4, 4, 2, 2, 16, 4),  // 128 threads
-    E(2, 32, 64, 16, 4, 4, 2, 2, 16, 4),
-    E(2, 64, 32, 16, 4, 4, 2, 2, 16, 3),
-    E(2, 32, 64, 8, 4, 4, 2, 2, 16, 4),
+    E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),  // TD product
+    E(3, 32, 32, 16, 2, 2, 2, 2, 16, 3),
+    E(3, 32, 32, 8, 2, 2, 3, 1, 16, 3),
+    E(3, 32, 32, 8, 2, 2, 2, 1, 16, 3),
+    E(3, 16, 64, 16, 1, 4, 2, 1, 16, 3),
+    E(3, 64, 16, 16, 4, 1, 2, 1, 16, 3),
+    E(3, 32, 32, 32, 2, 2, 2, 1, 16, 3),
+    E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),  // QD product
+    E(4, 16, 32, 8, 1, 2, 3, 1, 16, 3),
+    E(4, 32, 16, 8, 2, 1, 2, 1, 16, 3),
+    E(4, 16, 32, 32, 1, 2, 2, 1, 16, 3),
+    E(4, 16, 64, 16, 1, 4, 2, 1, 16, 2),
 };
 }  // namespace
 
