@@ -69,6 +69,10 @@ def parse():
                          "this flag forces it at N == 1 with --dist)")
     ap.add_argument("--nccl-bcast", action="store_true",
                     help="N > 1: replicate B with NCCL broadcasts in K panels instead of the fused kernel")
+    ap.add_argument("--gather-mode", choices=["copy", "pull"], default="pull",
+                    help="fused all-gather: the GEMM's CTAs pull B's panels over peer memory (pull; progress "
+                         "guaranteed by construction) or the copy engines gather and flag them (copy; needs the "
+                         "peer copies to run on copy engines)")
     ap.add_argument("--pull-panel", type=int, default=256, help="fused all-gather: K rows per panel")
     ap.add_argument("--pull-chunk", type=int, default=2,
                     help="fused all-gather: rows per copy chunk (small chunks spread each panel over many CTAs)")
@@ -304,7 +308,8 @@ def run_mpfk(args, ws, rank, local):
         if slices is not None:
             # one kernel: pull B's panels from the ranks' slices while computing
             ev_mid.record(stream)
-            launches[0] += slices.step(W, dA, dB, dC, rows, n, k, args.pull_panel, args.pull_chunk, stream)
+            launches[0] += slices.step(W, dA, dB, dC, rows, n, k, args.pull_panel, args.pull_chunk, stream,
+                                       mode=args.gather_mode)
             return ev_mid
         if overlap:
             # B broadcast in K panels, each panel's GEMM gated on its own panel
@@ -437,7 +442,10 @@ def run_mpfk(args, ws, rank, local):
         parallelism = f"row-shard x{ws}"
         if fused_note:
             parallelism += f" [{fused_note}]"
-        if slices is not None:
+        if slices is not None and args.gather_mode == "copy":
+            parallelism += (" + fused all-gather->GEMM (copy engines gather B's K panels from the peers' slices, "
+                            "one GEMM launch waits per panel on stream-memory flags)")
+        elif slices is not None:
             parallelism += " + fused all-gather->GEMM (B pulled over peer memory inside the GEMM kernel)"
         elif overlap:
             parallelism += f" + NCCL broadcast of B in {args.panels} K panels overlapped with the GEMM"

@@ -204,6 +204,20 @@ int mpfk_gemm_device_pull(int width, uint64_t m, uint64_t n, uint64_t k, const d
                           double *C, uint64_t ldc, uint64_t c_plane, int nsrc,
                           const double *const *src, const uint64_t *src_row0, uint64_t panel_rows,
                           uint64_t chunk_rows, void *stream, int *launches);
+/* All-gather -> GEMM with the copy engines doing the gather: B's K panels
+ * are copied from the source slices (peer or IPC-mapped memory; same table
+ * as mpfk_gemm_device_pull, up to 64 slices) into the local B on an
+ * internal stream, each followed by a stream memory write of the panel's
+ * flag, while ONE GEMM launch on `stream` waits per panel inside the kernel
+ * -- the transfer overlaps the FP64 work tile by tile and costs no SM time.
+ * Bit-identical to mpfk_gemm_device; after the call (in stream order) B
+ * holds the whole matrix.  panel_rows: a multiple of 16.  Without stream
+ * memory operations the gather completes before a plain GEMM launch. */
+int mpfk_gemm_device_gathered(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                              uint64_t lda, uint64_t a_plane, double *B, uint64_t ldb,
+                              uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, int nsrc,
+                              const double *const *src, const uint64_t *src_row0,
+                              uint64_t panel_rows, void *stream, int *launches);
 /* device memory and CUDA IPC plumbing for the fused path (one process per
  * GPU): handles are 64-byte cudaIpcMemHandle_t blobs. */
 int mpfk_device_alloc(uint64_t bytes, void **ptr);

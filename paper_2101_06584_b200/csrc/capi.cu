@@ -128,6 +128,10 @@ struct Device {
   size_t capA = 0, capB = 0, capC = 0;
   unsigned* gate = nullptr;  // gated path: K-panel flags + row-band tile counters
   size_t gate_cap = 0;
+  cudaStream_t gather = nullptr;   // copy-engine all-gather of B (mpfk_gemm_device_gathered)
+  cudaEvent_t evG[3] = {};         // gate reset, gather done, last use of ggate finished
+  unsigned* ggate = nullptr;       // its flags/counters (cudaMalloc'd: stream memory operations
+  size_t ggate_cap = 0;            // reject stream-ordered pool memory)
   Stager stage;  // pageable host operands
 };
 
@@ -157,6 +161,8 @@ std::mutex g_mu;
 // reference's).  Device-resident entry points run on the caller's stream and
 // take no lock.
 std::mutex g_call_mu;
+// mpfk_gemm_device_gathered: per-device flag buffer and gather stream
+std::mutex g_gather_mu;
 std::vector<Device> g_dev;
 int g_ndev = -1;
 
@@ -242,6 +248,8 @@ void ensure_devices(int n, int first = 0) {
     ck(cudaStreamCreateWithFlags(&D.up, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&D.down, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&D.stream2, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&D.gather, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : D.evG) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     for (auto& e : D.evB) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&D.evJ, cudaEventDisableTiming), "cudaEventCreate");
     for (auto& e : D.ev) ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -886,6 +894,7 @@ void mpfk_shutdown(void) {
     if (D.dB) cudaFree(D.dB);
     if (D.dC) cudaFree(D.dC);
     if (D.gate) cudaFree(D.gate);
+    if (D.ggate) cudaFree(D.ggate);
     for (auto& e : D.ev) cudaEventDestroy(e);
     for (auto& e : D.evA) cudaEventDestroy(e);
     for (auto& e : D.evC) cudaEventDestroy(e);
@@ -893,6 +902,8 @@ void mpfk_shutdown(void) {
     cudaStreamDestroy(D.up);
     cudaStreamDestroy(D.down);
     cudaStreamDestroy(D.stream2);
+    cudaStreamDestroy(D.gather);
+    for (auto& e : D.evG) cudaEventDestroy(e);
     for (auto& e : D.evB) cudaEventDestroy(e);
     cudaEventDestroy(D.evJ);
     D.stage.release();
@@ -1251,6 +1262,109 @@ int mpfk_gemm_device_pull(int width, uint64_t m, uint64_t n, uint64_t k, const d
       ck(cudaFreeAsync(ctr, s), "cudaFreeAsync");
     } else {
       l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, s);
+    }
+    count_matmul(m, n, k);
+    if (launches) *launches = l;
+  });
+}
+
+int mpfk_gemm_device_gathered(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                              uint64_t a_plane, double* B, uint64_t ldb, uint64_t b_plane, double* C, uint64_t ldc,
+                              uint64_t c_plane, int nsrc, const double* const* src, const uint64_t* src_row0,
+                              uint64_t panel_rows, void* stream, int* launches) {
+  return guarded([&] {
+    check_width(width);
+    if (nsrc < 1 || nsrc > 64) fail(MPFK_EINVAL, "mpfk: 1..64 source slices");
+    if (!src || !src_row0) fail(MPFK_EINVAL, "mpfk: null source table");
+    if (src_row0[0] != 0 || src_row0[nsrc] != k) fail(MPFK_EINVAL, "mpfk: source slices must cover rows [0, k)");
+    for (int s_ = 0; s_ < nsrc; ++s_)
+      if (src_row0[s_ + 1] < src_row0[s_]) fail(MPFK_EINVAL, "mpfk: source slices out of order");
+    if (panel_rows < 16 || panel_rows % 16) fail(MPFK_EINVAL, "mpfk: panel_rows must be a positive multiple of 16");
+    if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
+    if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
+      fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+      fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    Device& D = g_dev[dev];
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // panel p of B = rows [p*panel_rows, ...) gathered from the slices that
+    // hold them, whole rows of ldb doubles per plane
+    // A slice on this very device is copied in stream order BEFORE the GEMM:
+    // device-local copies may run as copy kernels, which a GEMM that fills
+    // every SM slot while it waits on panel flags would starve.  Slices on
+    // other GPUs move over NVLink on the copy engines, concurrently.
+    std::vector<char> local(nsrc, 0);
+    for (int s_ = 0; s_ < nsrc; ++s_) {
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, src[s_]) != cudaSuccess) {
+        cudaGetLastError();
+        local[s_] = 1;  // unknown: the safe side
+      } else {
+        local[s_] = at.type != cudaMemoryTypeDevice || at.device == g_dev[dev].id;
+      }
+    }
+    auto copy_panel = [&](uint64_t k0, uint64_t k1, cudaStream_t cs, int which) {  // which: 1 local, 0 remote, -1 all
+      for (int s_ = 0; s_ < nsrc; ++s_) {
+        if (which >= 0 && local[s_] != which) continue;
+        const uint64_t a = std::max(k0, src_row0[s_]), b = std::min(k1, src_row0[s_ + 1]);
+        if (a >= b) continue;
+        const uint64_t rows_s = src_row0[s_ + 1] - src_row0[s_];
+        for (int w = 0; w < width; ++w)
+          ck(cudaMemcpyAsync(B + w * b_plane + a * ldb, src[s_] + w * rows_s * ldb + (a - src_row0[s_]) * ldb,
+                             sizeof(double) * (b - a) * ldb, cudaMemcpyDefault, cs),
+             "gather copy");
+      }
+    };
+    int l = 0;
+    if (!(m && n && k) || !memops_available()) {
+      // no stream memory operations: gather everything, then the plain GEMM
+      if (m && n)
+        for (uint64_t k0 = 0; k0 < k; k0 += panel_rows) copy_panel(k0, std::min(k, k0 + panel_rows), s, -1);
+      l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, s);
+    } else {
+      if (m > 0x7fffffffULL || n > 0x7fffffffULL || k > 0x7fffffffULL)
+        fail(MPFK_EINVAL, "mpfk: dimension exceeds 2^31-1");
+      const uint64_t npan = (k + panel_rows - 1) / panel_rows, band_rows = 256, nb = (m + band_rows - 1) / band_rows;
+      // one flag buffer per device: the previous gathered GEMM on this device
+      // must be done with it (host wait; consecutive calls are whole GEMMs)
+      std::lock_guard<std::mutex> lk(g_gather_mu);
+      ck(cudaEventSynchronize(D.evG[2]), "previous gathered GEMM");
+      const size_t gbytes = sizeof(unsigned) * (npan + nb);
+      if (gbytes > D.ggate_cap) {
+        if (D.ggate) cudaFree(D.ggate);
+        D.ggate = nullptr;
+        D.ggate_cap = 0;
+        ck(cudaMalloc(reinterpret_cast<void**>(&D.ggate), gbytes), "cudaMalloc(gather gate)");
+        D.ggate_cap = gbytes;
+      }
+      unsigned* gate = D.ggate;
+      ck(cudaMemsetAsync(gate, 0, gbytes, s), "cudaMemsetAsync");
+      copy_panel(0, k, s, 1);  // this device's own rows, before the launch
+      ck(cudaEventRecord(D.evG[0], s), "event");
+      // the copy engines gather B panel by panel on the device's gather
+      // stream, flagging each panel; the GEMM on the caller's stream waits
+      // per panel inside the kernel (kern::GateArgs)
+      ck(cudaStreamWaitEvent(D.gather, D.evG[0], 0), "wait gate reset");
+      for (uint64_t p = 0; p < npan; ++p) {
+        copy_panel(p * panel_rows, std::min(k, (p + 1) * panel_rows), D.gather, 0);
+        cu_ck(g_write32(reinterpret_cast<CUstream>(D.gather), reinterpret_cast<CUdeviceptr>(gate + p), 1, 0),
+              "cuStreamWriteValue32");
+      }
+      ck(cudaEventRecord(D.evG[1], D.gather), "event");
+      kern::GemmArgs g;
+      g.A = A, g.B = B, g.C = C;
+      g.lda = (long long)lda, g.ldb = (long long)ldb, g.ldc = (long long)ldc;
+      g.pa = (long long)a_plane, g.pb = (long long)b_plane, g.pc = (long long)c_plane;
+      g.M = (int)m, g.N = (int)n, g.K = (int)k;
+      g.accumulate = 0;
+      g.batch = 1, g.sa = g.sb = g.sc = 0;
+      kern::GateArgs gate_args{gate, gate + npan, (int)panel_rows, (int)band_rows};
+      dispatch_gemm_gated(width, g, gate_args, s);
+      l = 1;
+      ck(cudaStreamWaitEvent(s, D.evG[1], 0), "join gather");  // B complete when the stream is
+      ck(cudaEventRecord(D.evG[2], s), "event");
     }
     count_matmul(m, n, k);
     if (launches) *launches = l;

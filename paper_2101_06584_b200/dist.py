@@ -291,13 +291,23 @@ class PeerBSlices:
         if a.size:
             L.memcpy(self.local, a.ctypes.data, a.nbytes)
 
-    def step(self, W, dA, dB, dC, rows, n, k, panel_rows=256, chunk_rows=2, stream=None) -> int:
-        """C_shard = A_shard * B with B pulled from the slices inside the GEMM."""
+    def step(self, W, dA, dB, dC, rows, n, k, panel_rows=256, chunk_rows=2, stream=None, mode="pull") -> int:
+        """C_shard = A_shard * B with B gathered from the slices while ONE GEMM
+        launch computes: mode "copy" -- the copy engines copy B's panels and
+        flag them, the kernel waits per panel (mpfk_gemm_device_gathered);
+        mode "pull" -- the GEMM's own CTAs pull the panels over peer memory
+        (mpfk_gemm_device_pull)."""
         from . import linalg as L
         if rows == 0:
             return 0
         s = stream.cuda_stream if stream is not None else 0
         lda, ldb, ldc = dA.shape[2], dB.shape[2], dC.shape[2]
+        if mode == "copy":
+            return L.gemm_device_gathered(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
+                                          dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, self.ptrs,
+                                          self.cuts, panel_rows, s)
+        if mode != "pull":
+            raise ValueError("PeerBSlices.step: mode must be 'copy' or 'pull'")
         return L.gemm_device_pull(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
                                   dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, self.ptrs, self.cuts,
                                   panel_rows, chunk_rows, s)

@@ -476,6 +476,22 @@ def gemm_device_pull(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_pla
     return launches.value
 
 
+def gemm_device_gathered(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int,
+                         ldb: int, b_plane: int, C_ptr: int, ldc: int, c_plane: int, src_ptrs, src_row0,
+                         panel_rows: int = 256, stream: int = 0) -> int:
+    """All-gather -> GEMM with the copy engines gathering B's panels from the
+    source slices while ONE gated GEMM launch computes
+    (mpfk_gemm_device_gathered); B_ptr receives the whole B."""
+    ns = len(src_ptrs)
+    srcs = (C.c_void_p * ns)(*src_ptrs)
+    rows = (C.c_uint64 * (ns + 1))(*src_row0)
+    launches = C.c_int(0)
+    N.check(N.lib().mpfk_gemm_device_gathered(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
+                                              c_plane, ns, srcs, rows, panel_rows, stream or None,
+                                              C.byref(launches)))
+    return launches.value
+
+
 def ipc_handle(dev_ptr: int) -> bytes:
     """The 64-byte CUDA IPC handle of a libmpfk device allocation."""
     buf = (C.c_char * 64)()

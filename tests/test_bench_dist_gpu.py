@@ -36,13 +36,15 @@ def test_torchrun_collective_path(gpu_lib, workload):
 
 
 @pytest.mark.gpu
-def test_torchrun_fused_allgather_path(gpu_lib):
-    """--fused-allgather with one rank: the GEMM pulls B from the rank's slice
-    inside the kernel; the result equals the one-shot GEMM."""
+@pytest.mark.parametrize("mode", ["copy", "pull"])
+def test_torchrun_fused_allgather_path(gpu_lib, mode):
+    """--fused-allgather with one rank: B gathered from the rank's slice
+    while one GEMM launch computes (copy engines + flags, or in-kernel
+    pulls); the result equals the one-shot GEMM."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--workload", "td1024",
            "--steps", "2", "--warmup", "1", "--no-e2e", "--no-cpu-baseline", "--dist", "--check",
-           "--fused-allgather", "--pull-panel", "64", "--pull-chunk", "8"]
+           "--fused-allgather", "--gather-mode", mode, "--pull-panel", "64", "--pull-chunk", "8"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])

@@ -24,7 +24,7 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, W, m, k, n, q):
+def _rank(rank, world, port, W, m, k, n, mode, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch
@@ -47,7 +47,7 @@ def _rank(rank, world, port, W, m, k, n, q):
         dA = torch.from_numpy(A.data).cuda()
         dB = torch.zeros((W, k, ld), dtype=torch.float64, device="cuda")
         dC = torch.zeros((W, max(rows, 1), ld), dtype=torch.float64, device="cuda")
-        launches = slices.step(W, dA, dB, dC, rows, n, k, panel_rows=64, chunk_rows=8)
+        launches = slices.step(W, dA, dB, dC, rows, n, k, panel_rows=64, chunk_rows=8, mode=mode)
         torch.cuda.synchronize()
         q.put((rank, r0, r1, dC[:, :rows].cpu().numpy(), dB.cpu().numpy(), launches))
         dist.barrier()  # nobody unmaps a slice another rank may still read
@@ -56,14 +56,15 @@ def _rank(rank, world, port, W, m, k, n, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["copy", "pull"])
 @pytest.mark.parametrize("W,m,k,n", [(2, 96, 200, 70), (4, 50, 131, 33)])
-def test_two_process_ipc_fused_allgather(gpu_lib, W, m, k, n):
+def test_two_process_ipc_fused_allgather(gpu_lib, W, m, k, n, mode):
     import oracle as O
     P = gpu_lib
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, W, m, k, n, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, W, m, k, n, mode, q)) for r in range(2)]
     for p in procs:
         p.start()
     got = [q.get(timeout=300) for _ in range(2)]
