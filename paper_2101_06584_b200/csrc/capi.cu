@@ -105,7 +105,7 @@ __global__ void selftest_kernel(const double* in, int* ok) {
   *ok = (rn ? 1 : 0) | (fused ? 2 : 0);
 }
 
-constexpr int kMaxChunks = 8;
+constexpr int kMaxChunks = 16;  // row chunks / K panels of a host-buffer GEMM
 
 #include "host_stage.inl"
 

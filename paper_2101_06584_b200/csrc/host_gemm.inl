@@ -214,7 +214,8 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   if (W == 3) sBM = Cfg3::BM, sBN = Cfg3::BN, sMINB = Cfg3::MINB;
   if (W == 4) sBM = Cfg4::BM, sBN = Cfg4::BN, sMINB = Cfg4::MINB;
   auto split = [](uint64_t rows, uint64_t min_rows) {
-    const uint64_t nc = std::max<uint64_t>(1, std::min<uint64_t>(kMaxChunks, rows / std::max<uint64_t>(min_rows, 1)));
+    // at most 8 uniform chunks (chunk_bounds may halve the first and last)
+    const uint64_t nc = std::max<uint64_t>(1, std::min<uint64_t>(8, rows / std::max<uint64_t>(min_rows, 1)));
     const uint64_t crows = ((rows + nc - 1) / nc + 63) / 64 * 64;
     return std::make_pair((rows + crows - 1) / std::max<uint64_t>(crows, 1), crows);
   };
@@ -234,6 +235,27 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     if (copy_s > 0.3 * kern_s)
       return split(rows, (uint64_t)std::ceil(sms * 1.5 / std::max(double(tiles_per_band) / sBM, 1e-9)));
     return split(rows, rows);
+  };
+  // Row boundaries of a shard's chunks.  Large shards (the >= 4-tiles-per-SM
+  // rule) get a half-size first and last chunk: the first GEMM starts after
+  // half the A rows, and the download left exposed after the last GEMM is
+  // half a chunk.
+  auto chunk_bounds = [&](uint64_t rows) {
+    const auto pr = chunks_of(rows);
+    const uint64_t nc = pr.first, crows = pr.second;
+    std::vector<uint64_t> b{0};
+    const double big = double(n) / (64.0 * 64.0);
+    const uint64_t min_rows = (uint64_t)std::ceil(sms * 4.0 / std::max(big, 1e-9));
+    if (nc >= 2 && rows >= 2 * min_rows && crows >= 128) {
+      const uint64_t h = crows / 2 / 64 * 64;
+      b.push_back(h);
+      while (b.back() + crows < rows) b.push_back(b.back() + crows);
+    } else {
+      for (uint64_t c = 1; c < nc; ++c) b.push_back(std::min(rows, c * crows));
+    }
+    if (b.back() < rows) b.push_back(rows);
+    if (rows == 0) b.push_back(0);
+    return b;
   };
   // Single GPU: B is uploaded in K panels right after the first A chunk, and
   // the first chunk's GEMM runs panel by panel (continuing the chains from C,
@@ -265,11 +287,13 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   for (int g = 0; g < G; ++g) g_dev[sh[g].dev].stage.reset();
 
   std::vector<int> nchunks(G, 0);
+  std::vector<std::vector<uint64_t>> bounds(G);
+  for (int g = 0; g < G; ++g) bounds[g] = chunk_bounds(sh[g].r1 - sh[g].r0);
   auto upload_a = [&](int g, int c) {  // A row chunk c of shard g
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
-    const uint64_t rows = s.r1 - s.r0, crows = chunks_of(rows).second;
-    const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
+    const uint64_t rows = s.r1 - s.r0;
+    const uint64_t c0 = bounds[g][c], c1 = bounds[g][c + 1];
     for (int w = 0; w < W; ++w)
       copy_h2d(D, a_pin, D.dA + w * rows * lda + c0 * lda, lda, A->base + w * pa_h + (s.r0 + c0) * A->stride,
           A->stride, K, c1 - c0, D.up);
@@ -281,10 +305,10 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   // after all uploads (with page-locked buffers the copies are asynchronous
   // and the order of the calls does not matter).
   const bool defer_a = G == 1 && !a_pin;
-  const bool panel_split0 = !(fast && splitk_plan(W, std::min<uint64_t>(m, chunks_of(m).second), n, K).S > 1);
+  const bool panel_split0 = !(fast && splitk_plan(W, bounds[0][1], n, K).S > 1);
   const bool early0 = G == 1 && !b_pin && panels_of(K).first > 1 && panel_split0;
   auto gemm_chunk0_panel = [&](Device& D, int p) {
-    const uint64_t rows = m, crows = chunks_of(rows).second, c1 = std::min<uint64_t>(rows, crows);
+    const uint64_t rows = m, c1 = bounds[0][1];
     const uint64_t pk = panels_of(K).second, k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
     if (p == 0) ck(cudaStreamWaitEvent(D.stream, D.evA[0], 0), "wait A chunk");
     ck(cudaStreamWaitEvent(D.stream, D.evB[p], 0), "wait B panel");
@@ -299,7 +323,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(rows * lda, 1));
     grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
     grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(rows * ldc, 1));
-    nchunks[g] = rows ? (int)chunks_of(rows).first : 0;
+    nchunks[g] = rows ? (int)bounds[g].size() - 1 : 0;
     ck(cudaEventRecord(D.ev[0], D.up), "event");
     if (early0) ck(cudaEventRecord(D.ev[2], D.stream), "event");
     if (nchunks[g]) upload_a(g, 0);
@@ -322,8 +346,8 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   auto download = [&](int g, int c) {  // C row chunk c of shard g, after its GEMM
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
-    const uint64_t rows = s.r1 - s.r0, crows = chunks_of(rows).second;
-    const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
+    const uint64_t rows = s.r1 - s.r0;
+    const uint64_t c0 = bounds[g][c], c1 = bounds[g][c + 1];
     ck(cudaStreamWaitEvent(D.down, D.evC[c], 0), "wait C chunk");
     for (int w = 0; w < W; ++w)
       copy_d2h(D, c_pin, C->base + w * pc_h + (s.r0 + c0) * C->stride, C->stride, D.dC + w * rows * ldc + c0 * ldc,
@@ -350,13 +374,12 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
       ck(cudaEventRecord(D.ev[5], D.stream), "event");  // B complete on this GPU
     }
     const cudaEvent_t b_ready = peer ? D.ev[5] : D.ev[1];
-    const uint64_t crows = nchunks[g] ? chunks_of(rows).second : 0;
     const auto ppair = panels_of(K);
     const int np = ppair.first;
     const uint64_t pk = ppair.second;
     for (int c = 0; c < nchunks[g]; ++c) {
       cudaStream_t cs = (c & 1) ? D.stream2 : D.stream;
-      const uint64_t c0 = c * crows, c1 = std::min<uint64_t>(rows, c0 + crows);
+      const uint64_t c0 = bounds[g][c], c1 = bounds[g][c + 1];
       if (defer_a && c > 0) upload_a(g, c);
       ck(cudaStreamWaitEvent(cs, D.evA[c], 0), "wait A chunk");
       if (c == 0 && early0) {
