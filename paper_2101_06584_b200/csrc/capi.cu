@@ -161,8 +161,8 @@ std::mutex g_mu;
 // reference's).  Device-resident entry points run on the caller's stream and
 // take no lock.
 std::mutex g_call_mu;
-// mpfk_gemm_device_gathered: per-device flag buffer and gather stream
-std::mutex g_gather_mu;
+// mpfk_gemm_device_gathered: one lock per device for its flag buffer
+std::mutex g_gather_mu[64];
 std::vector<Device> g_dev;
 int g_ndev = -1;
 
@@ -1329,7 +1329,7 @@ int mpfk_gemm_device_gathered(int width, uint64_t m, uint64_t n, uint64_t k, con
       const uint64_t npan = (k + panel_rows - 1) / panel_rows, band_rows = 256, nb = (m + band_rows - 1) / band_rows;
       // one flag buffer per device: the previous gathered GEMM on this device
       // must be done with it (host wait; consecutive calls are whole GEMMs)
-      std::lock_guard<std::mutex> lk(g_gather_mu);
+      std::lock_guard<std::mutex> lk(g_gather_mu[dev % 64]);
       ck(cudaEventSynchronize(D.evG[2]), "previous gathered GEMM");
       const size_t gbytes = sizeof(unsigned) * (npan + nb);
       if (gbytes > D.ggate_cap) {
