@@ -213,7 +213,8 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   int sBM = Cfg2s::BM, sBN = Cfg2s::BN, sMINB = Cfg2s::MINB;
   if (W == 3) sBM = Cfg3::BM, sBN = Cfg3::BN, sMINB = Cfg3::MINB;
   if (W == 4) sBM = Cfg4::BM, sBN = Cfg4::BN, sMINB = Cfg4::MINB;
-  auto split = [](uint64_t rows, uint64_t min_rows) {
+  auto split = [](uint64_t rows, uint64_t min_rows) -> std::pair<uint64_t, uint64_t> {
+    if (rows == 0) return {0, 0};
     // at most 8 uniform chunks (chunk_bounds may halve the first and last)
     const uint64_t nc = std::max<uint64_t>(1, std::min<uint64_t>(8, rows / std::max<uint64_t>(min_rows, 1)));
     const uint64_t crows = ((rows + nc - 1) / nc + 63) / 64 * 64;
@@ -241,6 +242,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   // half the A rows, and the download left exposed after the last GEMM is
   // half a chunk.
   auto chunk_bounds = [&](uint64_t rows) {
+    if (rows == 0) return std::vector<uint64_t>{0, 0};  // an empty shard (G > row blocks / per)
     const auto pr = chunks_of(rows);
     const uint64_t nc = pr.first, crows = pr.second;
     std::vector<uint64_t> b{0};
@@ -254,7 +256,6 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
       for (uint64_t c = 1; c < nc; ++c) b.push_back(std::min(rows, c * crows));
     }
     if (b.back() < rows) b.push_back(rows);
-    if (rows == 0) b.push_back(0);
     return b;
   };
   // Single GPU: B is uploaded in K panels right after the first A chunk, and

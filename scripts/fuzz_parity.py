@@ -1,0 +1,100 @@
+"""Randomised parity sweep (one-off evidence, not a unit test): random widths,
+shapes, host-buffer kinds, device counts (MPFK_EMULATED_DEVICES), device
+entry points with offset windows, K-panel continuation, fused all-gather
+(pull and copy-engine variants) -- every result compared bit for bit with
+the reference build.  python scripts/fuzz_parity.py [cases] [seed]"""
+import os
+import sys
+
+os.environ.setdefault("MPFK_EMULATED_DEVICES", "3")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle as O  # noqa: E402
+import paper_2101_06584_b200 as P  # noqa: E402
+from tests.helpers import mismatches, random_signed  # noqa: E402
+
+cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+
+
+def dim():
+    return int(rng.choice([rng.integers(1, 20), rng.integers(20, 200), rng.integers(200, 900)]))
+
+
+bad = 0
+for t in range(cases):
+    W = int(rng.integers(2, 5))
+    m, n, k = dim(), dim(), dim()
+    A = random_signed(W, m, k, 1000 + t)
+    B = random_signed(W, k, n, 2000 + t)
+    want = O.ref_gemm(A, B, k, n)
+    kind = t % 5
+    if os.environ.get("FUZZ_VERBOSE"):
+        print(f"start {t} W={W} m={m} n={n} k={k} kind={kind}", flush=True)
+    if kind == 0:  # host API, pageable or pinned, 1..3 (emulated) devices
+        pinned = bool(rng.integers(0, 2))
+        Am = P.MPMatrix.from_planes(A[:, :, :k], pinned=pinned)
+        Bm = P.MPMatrix.from_planes(B[:, :, :n], pinned=pinned)
+        Cm = P.MPMatrix(W, m, n, pinned=pinned)
+        Cm.data[...] = 1.5
+        workers = int(rng.integers(1, 4))
+        if os.environ.get("FUZZ_VERBOSE"):
+            print(f"  host pinned={pinned} workers={workers}", flush=True)
+        P.matmul_block_parallel_into(Cm, Am, Bm, 32, P.KernelVariant.SIMD_LOADSTORE, workers)
+        got = Cm.data
+        what = f"host pinned={pinned}"
+    elif kind == 1:  # device API on offset windows
+        dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        ldc = n + 2 * int(rng.integers(0, 3)) + (n & 1)
+        dC = torch.full((W, m, ldc), 2.5, dtype=torch.float64, device="cuda")
+        P.gemm_device(W, m, n, k, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), B.shape[2],
+                      k * B.shape[2], dC.data_ptr(), ldc, m * ldc)
+        got = dC.cpu().numpy()[:, :, :n]
+        want = want[:, :, :n]
+        what = "device"
+    elif kind == 2:  # K-panel continuation at a random even split
+        dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        ld = B.shape[2]
+        dC = torch.zeros((W, m, ld), dtype=torch.float64, device="cuda")
+        h = int(rng.integers(0, k // 2 + 1)) * 2 if k > 1 else 0
+        P.gemm_device(W, m, n, h, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), ld, k * ld,
+                      dC.data_ptr(), ld, m * ld)
+        P.gemm_device_acc(W, m, n, k - h, dA.data_ptr() + 8 * h, A.shape[2], m * A.shape[2],
+                          dB.data_ptr() + 8 * h * ld, ld, k * ld, dC.data_ptr(), ld, m * ld)
+        got = dC.cpu().numpy()
+        what = f"continuation h={h}"
+        if h == 0:  # a 0-length first panel leaves C = +0; the continuation then is not the product
+            continue
+    else:  # fused all-gather, random slice cuts
+        ns = int(rng.integers(1, min(8, k) + 1))
+        cuts = sorted(set([0, k] + [int(x) for x in rng.integers(0, k + 1, size=ns - 1)]))
+        ld = B.shape[2]
+        dA = torch.from_numpy(A).cuda()
+        sl = [torch.from_numpy(np.ascontiguousarray(B[:, a:b])).cuda() for a, b in zip(cuts, cuts[1:])]
+        dB = torch.full((W, k, ld), float("nan"), dtype=torch.float64, device="cuda")
+        dC = torch.zeros((W, m, ld), dtype=torch.float64, device="cuda")
+        pr = 16 * int(rng.integers(1, 9))
+        ptrs = [t_.data_ptr() if t_.numel() else dA.data_ptr() for t_ in sl]
+        if kind == 3:
+            P.gemm_device_pull(W, m, n, k, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), ld, k * ld,
+                               dC.data_ptr(), ld, m * ld, ptrs, cuts, pr, int(rng.integers(1, 9)))
+            what = f"pull cuts={cuts} panel={pr}"
+        else:
+            P.gemm_device_gathered(W, m, n, k, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), ld,
+                                   k * ld, dC.data_ptr(), ld, m * ld, ptrs, cuts, pr)
+            what = f"gathered cuts={cuts} panel={pr}"
+        torch.cuda.synchronize()
+        got = dC.cpu().numpy()
+    torch.cuda.synchronize()
+    if os.environ.get("FUZZ_VERBOSE"):
+        print(f"case {t} W={W} m={m} n={n} k={k} {what}", flush=True)
+    mm = mismatches(got, want)
+    if mm:
+        bad += 1
+        print(f"MISMATCH case {t}: W={W} m={m} n={n} k={k} {what}: {mm} cells", flush=True)
+print(f"{cases} cases, {bad} with mismatches")
+sys.exit(1 if bad else 0)

@@ -21,8 +21,9 @@ import numpy as np
 import oracle as O
 import paper_2101_06584_b200 as P
 out = {"devices": P.device_count(), "cases": []}
+# (3, 194, ...) with 3 devices: 128-row spans leave the third shard empty
 for W, m, n, k, workers in [(2, 300, 129, 77, 3), (3, 200, 64, 300, 2), (4, 130, 33, 47, 3), (2, 700, 260, 1030, 3),
-                            (3, 5, 9, 11, 3)]:
+                            (3, 5, 9, 11, 3), (3, 194, 463, 367, 3)]:
     A = P.fill_baseline(W, m, k, 1, wide=True)
     B = P.fill_baseline(W, k, n, 2, wide=True)
     C = P.MPMatrix(W, m, n)
@@ -67,6 +68,7 @@ def test_multi_device_host_path_emulated(gpu_lib, emulated):
         g = min(c["workers"], emulated, (c["m"] + 63) // 64)
         assert c["n_gpus"] == g, c
         assert (c["peer_bytes"] > 0) == (g > 1), c
+    assert any(c["m"] == 194 and c["n_gpus"] == emulated for c in out["cases"]) or emulated < 3
     assert out["gemm_all_devices"] == emulated
     assert out["gemm_same"]
     assert out["fast_deterministic"] and out["fast_close"]
