@@ -289,7 +289,15 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
 
   std::vector<int> nchunks(G, 0);
   std::vector<std::vector<uint64_t>> bounds(G);
-  for (int g = 0; g < G; ++g) bounds[g] = chunk_bounds(sh[g].r1 - sh[g].r0);
+  // MPFK_FAST splits K only for a shard whose whole output cannot fill the
+  // GPU (the same decision mpfk_splitk_segments reports for its shape); such
+  // a shard runs as one chunk, every other shard is bit-exact
+  std::vector<char> fast_split(G, 0);
+  for (int g = 0; g < G; ++g) {
+    const uint64_t rows = sh[g].r1 - sh[g].r0;
+    fast_split[g] = fast && rows && splitk_plan(W, rows, n, K).S > 1;
+    bounds[g] = fast_split[g] ? std::vector<uint64_t>{0, rows} : chunk_bounds(rows);
+  }
   auto upload_a = [&](int g, int c) {  // A row chunk c of shard g
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
@@ -306,7 +314,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   // after all uploads (with page-locked buffers the copies are asynchronous
   // and the order of the calls does not matter).
   const bool defer_a = G == 1 && !a_pin;
-  const bool panel_split0 = !(fast && splitk_plan(W, bounds[0][1], n, K).S > 1);
+  const bool panel_split0 = !fast_split[0];
   const bool early0 = G == 1 && !b_pin && panels_of(K).first > 1 && panel_split0;
   auto gemm_chunk0_panel = [&](Device& D, int p) {
     const uint64_t rows = m, c1 = bounds[0][1];
@@ -385,7 +393,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
       ck(cudaStreamWaitEvent(cs, D.evA[c], 0), "wait A chunk");
       if (c == 0 && early0) {
         // enqueued panel by panel in phase1
-      } else if (fast && splitk_plan(W, c1 - c0, n, K).S > 1) {
+      } else if (fast_split[g]) {  // one chunk: the whole shard
         ck(cudaStreamWaitEvent(cs, b_ready, 0), "wait B");
         launches[g] += enqueue_gemm_fast(W, c1 - c0, n, K, D.dA + c0 * lda, lda, rows * lda, D.dB, ldb,
                                          K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs);

@@ -32,7 +32,7 @@ for t in range(cases):
     A = random_signed(W, m, k, 1000 + t)
     B = random_signed(W, k, n, 2000 + t)
     want = O.ref_gemm(A, B, k, n)
-    kind = t % 5
+    kind = t % 8
     if os.environ.get("FUZZ_VERBOSE"):
         print(f"start {t} W={W} m={m} n={n} k={k} kind={kind}", flush=True)
     if kind == 0:  # host API, pageable or pinned, 1..3 (emulated) devices
@@ -69,7 +69,38 @@ for t in range(cases):
         what = f"continuation h={h}"
         if h == 0:  # a 0-length first panel leaves C = +0; the continuation then is not the product
             continue
+    elif kind == 5:  # Strassen (host API) at a random cutoff
+        cut = int(rng.choice([8, 16, 32, 64, 128]))
+        Am = P.MPMatrix.from_planes(A[:, :, :k])
+        Bm = P.MPMatrix.from_planes(B[:, :, :n])
+        got = P.matmul_strassen(Am, Bm, cutoff=cut).data
+        want = O.ref_strassen(A, B, k, n, cutoff=cut)
+        what = f"strassen cutoff={cut}"
+    elif kind == 6:  # elementwise on an m x n pair
+        op = ["add", "mul", "add_merge"][int(rng.integers(0, 3 if W == 3 else 2))]
+        X = random_signed(W, m, n, 3000 + t)
+        Y = random_signed(W, m, n, 4000 + t)
+        Xm, Ym = P.MPMatrix.from_planes(X[:, :, :n]), P.MPMatrix.from_planes(Y[:, :, :n])
+        out = P.MPMatrix(W, m, n)
+        P.ew_apply_into(out, Xm, Ym, {"add": P.EwOp.add, "mul": P.EwOp.mul, "add_merge": P.EwOp.add_merge}[op],
+                        P.KernelVariant.SIMD_LOADSTORE)
+        got = out.data
+        want = O.ref_ew(W, op, X, Y, n, variant=2)
+        what = f"ew {op}"
+    elif kind == 7:  # MPFK_FAST: the bit-exact path where no split is planned, deterministic where it is
+        Am = P.MPMatrix.from_planes(A[:, :, :k], pinned=bool(rng.integers(0, 2)))
+        Bm = P.MPMatrix.from_planes(B[:, :, :n])
+        F1 = P.gemm(Am, Bm, flags=P.FAST)
+        if P.splitk_segments(W, m, n, k) > 1:
+            F2 = P.gemm(Am, Bm, flags=P.FAST)
+            if not P.bits_equal(F1, F2):
+                bad += 1
+                print(f"NONDETERMINISTIC FAST case {t}: W={W} m={m} n={n} k={k}", flush=True)
+            continue
+        got = F1.data
+        what = "fast (not split)"
     else:  # fused all-gather, random slice cuts
+        kind = 3 if kind == 3 else 4
         ns = int(rng.integers(1, min(8, k) + 1))
         cuts = sorted(set([0, k] + [int(x) for x in rng.integers(0, k + 1, size=ns - 1)]))
         ld = B.shape[2]
