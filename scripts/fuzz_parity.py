@@ -29,12 +29,12 @@ bad = 0
 for t in range(cases):
     W = int(rng.integers(2, 5))
     m, n, k = dim(), dim(), dim()
-    if t % 8 == 0 and rng.random() < 0.4:  # wide host problems: multi-chunk, half-size end chunks, staging pieces
+    if t % 9 == 0 and rng.random() < 0.4:  # wide host problems: multi-chunk, half-size end chunks, staging pieces
         m, n, k = int(rng.integers(1500, 3200)), int(rng.integers(1500, 3200)), int(rng.integers(1, 64))
     A = random_signed(W, m, k, 1000 + t)
     B = random_signed(W, k, n, 2000 + t)
     want = O.ref_gemm(A, B, k, n)
-    kind = t % 8
+    kind = t % 9
     if os.environ.get("FUZZ_VERBOSE"):
         print(f"start {t} W={W} m={m} n={n} k={k} kind={kind}", flush=True)
     if kind == 0:  # host API, pageable or pinned, 1..3 (emulated) devices
@@ -89,6 +89,16 @@ for t in range(cases):
         got = out.data
         want = O.ref_ew(W, op, X, Y, n, variant=2)
         what = f"ew {op}"
+    elif kind == 8:  # dist.matmul_sharded_into without a process group (host panels, gated continuation)
+        from paper_2101_06584_b200.dist import matmul_sharded_into
+        pinned = bool(rng.integers(0, 2))
+        Am = P.MPMatrix.from_planes(A[:, :, :k], pinned=pinned)
+        Bm = P.MPMatrix.from_planes(B[:, :, :n], pinned=pinned)
+        Cm = P.MPMatrix(W, m, n, pinned=pinned)
+        Cm.data[...] = 4.5
+        matmul_sharded_into(Cm, Am, Bm, panels=int(rng.integers(1, 9)), device=torch.device("cuda", 0))
+        got = Cm.data
+        what = f"sharded_into pinned={pinned}"
     elif kind == 7:  # MPFK_FAST: the bit-exact path where no split is planned, deterministic where it is
         Am = P.MPMatrix.from_planes(A[:, :, :k], pinned=bool(rng.integers(0, 2)))
         Bm = P.MPMatrix.from_planes(B[:, :, :n])
