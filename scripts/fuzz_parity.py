@@ -2,7 +2,7 @@
 shapes, host-buffer kinds, device counts (MPFK_EMULATED_DEVICES), device
 entry points with offset windows, K-panel continuation, fused all-gather
 (pull and copy-engine variants) -- every result compared bit for bit with
-the reference build.  python scripts/fuzz_parity.py [cases] [seed]"""
+the reference build.  python scripts/fuzz_parity.py [cases] [seed] [host threads]"""
 import os
 import sys
 
@@ -17,16 +17,13 @@ import oracle as O  # noqa: E402
 import paper_2101_06584_b200 as P  # noqa: E402
 from tests.helpers import mismatches, random_signed  # noqa: E402
 
-cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+def one_case(t, rng):
+    """case t with its own generator; returns the number of mismatching cases (0/1)"""
+    bad_here = 0
 
+    def dim():
+        return int(rng.choice([rng.integers(1, 20), rng.integers(20, 200), rng.integers(200, 900)]))
 
-def dim():
-    return int(rng.choice([rng.integers(1, 20), rng.integers(20, 200), rng.integers(200, 900)]))
-
-
-bad = 0
-for t in range(cases):
     W = int(rng.integers(2, 5))
     m, n, k = dim(), dim(), dim()
     if t % 9 == 0 and rng.random() < 0.4:  # wide host problems: multi-chunk, half-size end chunks, staging pieces
@@ -70,7 +67,7 @@ for t in range(cases):
         got = dC.cpu().numpy()
         what = f"continuation h={h}"
         if h == 0:  # a 0-length first panel leaves C = +0; the continuation then is not the product
-            continue
+            return 0
     elif kind == 5:  # Strassen (host API) at a random cutoff
         cut = int(rng.choice([8, 16, 32, 64, 128]))
         Am = P.MPMatrix.from_planes(A[:, :, :k])
@@ -106,9 +103,9 @@ for t in range(cases):
         if P.splitk_segments(W, m, n, k) > 1:
             F2 = P.gemm(Am, Bm, flags=P.FAST)
             if not P.bits_equal(F1, F2):
-                bad += 1
+                bad_here += 1
                 print(f"NONDETERMINISTIC FAST case {t}: W={W} m={m} n={n} k={k}", flush=True)
-            continue
+            return bad_here
         got = F1.data
         what = "fast (not split)"
     else:  # fused all-gather, random slice cuts
@@ -137,7 +134,36 @@ for t in range(cases):
         print(f"case {t} W={W} m={m} n={n} k={k} {what}", flush=True)
     mm = mismatches(got, want)
     if mm:
-        bad += 1
+        bad_here += 1
         print(f"MISMATCH case {t}: W={W} m={m} n={n} k={k} {what}: {mm} cells", flush=True)
-print(f"{cases} cases, {bad} with mismatches")
-sys.exit(1 if bad else 0)
+    return bad_here
+
+
+def run(cases, seed, threads=1):
+    """cases split over `threads` host threads calling the library at once"""
+    import threading
+    total = [0]
+    lock = threading.Lock()
+
+    def worker(i):
+        rng = np.random.default_rng([seed, i])
+        for t in range(i, cases, threads):
+            b = one_case(t, rng)
+            with lock:
+                total[0] += b
+
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(threads)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    return total[0]
+
+
+if __name__ == "__main__":
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    threads = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    bad = run(cases, seed, threads)
+    print(f"{cases} cases, {bad} with mismatches")
+    sys.exit(1 if bad else 0)
