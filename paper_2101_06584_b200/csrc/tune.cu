@@ -67,18 +67,12 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>}
 
 const Entry kEntries[] = {
-    E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),  // TD product
-    E(3, 32, 32, 16, 2, 2, 2, 2, 16, 3),
-    E(3, 32, 32, 8, 2, 2, 3, 1, 16, 3),
-    E(3, 32, 32, 8, 2, 2, 2, 1, 16, 3),
-    E(3, 16, 64, 16, 1, 4, 2, 1, 16, 3),
-    E(3, 64, 16, 16, 4, 1, 2, 1, 16, 3),
-    E(3, 32, 32, 32, 2, 2, 2, 1, 16, 3),
-    E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),  // QD product
-    E(4, 16, 32, 8, 1, 2, 3, 1, 16, 3),
-    E(4, 32, 16, 8, 2, 1, 2, 1, 16, 3),
-    E(4, 16, 32, 32, 1, 2, 2, 1, 16, 3),
-    E(4, 16, 64, 16, 1, 4, 2, 1, 16, 2),
+    E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
+    E(2, 64, 64, 24, 4, 4, 2, 2, 16, 2),
+    E(2, 64, 64, 24, 4, 4, 2, 3, 16, 2),
+    E(2, 64, 64, 16, 4, 4, 2, 4, 16, 2),
+    E(2, 64, 64, 32, 4, 4, 2, 2, 16, 1),
+    E(2, 64, 64, 8, 4, 4, 3, 2, 16, 2),
 };
 }  // namespace
 
