@@ -57,7 +57,10 @@ struct Fail {
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
     cudaGetLastError();  // clear sticky-free errors
-    fail(MPFK_ECUDA, std::string("mpfk: ") + what + ": " + cudaGetErrorString(e));
+    // device or pinned-host memory exhausted: the twin of std::bad_alloc
+    // (linalg.hpp:116), not a device failure
+    fail(e == cudaErrorMemoryAllocation ? MPFK_ENOMEM : MPFK_ECUDA,
+         std::string("mpfk: ") + what + ": " + cudaGetErrorString(e));
   }
 }
 

@@ -162,3 +162,14 @@ def test_gated_host_path_bitwise(gpu_lib, W, m, n, k, monkeypatch):
     want = O.ref_gemm(A.data, B.data, k, n)
     assert mismatches(Cg.data, want) == 0
     assert gated or k < 256  # these shapes are small enough for the gated path
+
+
+def test_out_of_memory_is_memory_error(gpu_lib):
+    """an impossible allocation maps to MPFK_ENOMEM -> MemoryError (the
+    reference's std::bad_alloc, linalg.hpp:116), and the library stays usable"""
+    P = gpu_lib
+    with pytest.raises(MemoryError):
+        P.device_alloc(1 << 50)
+    A = P.fill_baseline(2, 40, 30, 1)
+    B = P.fill_baseline(2, 30, 20, 2)
+    assert mismatches(P.matmul_block(A, B).data, O.ref_gemm(A.data, B.data, 30, 20)) == 0
