@@ -17,6 +17,20 @@ import oracle as O  # noqa: E402
 import paper_2101_06584_b200 as P  # noqa: E402
 from tests.helpers import mismatches, random_signed  # noqa: E402
 
+def structured(W, rows, cols, rng):
+    """planes of exactly representable values with many zero components:
+    leading components from {0, +-1, +-2^-j, +-(1 + 2^-52)}, the next
+    component 0 or a power of two far below, the rest 0 (normalized)"""
+    ld = (cols + 3) & ~3
+    a = np.zeros((W, rows, ld))
+    lead = rng.choice([0.0, 1.0, -1.0, 0.5, -0.25, 2.0 ** -20, 1.0 + 2.0 ** -52, -(1.0 + 2.0 ** -52)],
+                      size=(rows, cols))
+    a[0, :, :cols] = lead
+    tail = rng.choice([0.0, 2.0 ** -60, -(2.0 ** -70)], size=(rows, cols))
+    a[1, :, :cols] = np.where(lead != 0.0, tail, 0.0)
+    return a
+
+
 def one_case(t, rng):
     """case t with its own generator; returns the number of mismatching cases (0/1)"""
     bad_here = 0
@@ -28,8 +42,11 @@ def one_case(t, rng):
     m, n, k = dim(), dim(), dim()
     if t % 9 == 0 and rng.random() < 0.4:  # wide host problems: multi-chunk, half-size end chunks, staging pieces
         m, n, k = int(rng.integers(1500, 3200)), int(rng.integers(1500, 3200)), int(rng.integers(1, 64))
-    A = random_signed(W, m, k, 1000 + t)
-    B = random_signed(W, k, n, 2000 + t)
+    if rng.random() < 0.25:  # structured: exact small values, zero tails -> renorm5 / vseb zero-residual paths
+        A, B = structured(W, m, k, rng), structured(W, k, n, rng)
+    else:
+        A = random_signed(W, m, k, 1000 + t)
+        B = random_signed(W, k, n, 2000 + t)
     want = O.ref_gemm(A, B, k, n)
     kind = t % 9
     if os.environ.get("FUZZ_VERBOSE"):
