@@ -173,3 +173,29 @@ def test_out_of_memory_is_memory_error(gpu_lib):
     A = P.fill_baseline(2, 40, 30, 1)
     B = P.fill_baseline(2, 30, 20, 2)
     assert mismatches(P.matmul_block(A, B).data, O.ref_gemm(A.data, B.data, 30, 20)) == 0
+
+
+def test_shutdown_and_reinitialise(gpu_lib):
+    """mpfk_shutdown releases every device resource (streams, events, buffers,
+    staging ring, flag buffers); the next call initialises again and gives the
+    same bits, for the host, device, gated and staged paths"""
+    import torch
+    P = gpu_lib
+    W, m, n, k = 3, 300, 200, 700
+    A = P.fill_baseline(W, m, k, 5, wide=True, pinned=True)
+    B = P.fill_baseline(W, k, n, 6, wide=True, pinned=True)
+    Ap = P.fill_baseline(W, m, k, 5, wide=True)  # pageable copies
+    Bp = P.fill_baseline(W, k, n, 6, wide=True)
+    want = O.ref_gemm(A.data, B.data, k, n)
+    for _ in range(2):
+        C1 = P.MPMatrix(W, m, n, pinned=True)
+        P.matmul_block_parallel_into(C1, A, B)
+        C2 = P.matmul_block(Ap, Bp)
+        assert mismatches(C1.data, want) == 0 and mismatches(C2.data, want) == 0
+        dA, dB = torch.from_numpy(A.data).cuda(), torch.from_numpy(B.data).cuda()
+        dC = torch.zeros((W, m, B.stride()), dtype=torch.float64, device="cuda")
+        P.gemm_device(W, m, n, k, dA.data_ptr(), A.stride(), m * A.stride(), dB.data_ptr(), B.stride(),
+                      k * B.stride(), dC.data_ptr(), B.stride(), m * B.stride())
+        torch.cuda.synchronize()
+        assert mismatches(dC.cpu().numpy(), want) == 0
+        N.lib().mpfk_shutdown()
