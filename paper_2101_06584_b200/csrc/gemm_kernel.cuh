@@ -17,6 +17,12 @@
 // cp.async (LDGSTS) in a STAGES-deep ring; operand traffic is tiny next to
 // the 20-218 FP64 operations per multiply-add, so the kernel is bound by the
 // FP64 pipe, not by HBM, L2 or shared memory.
+//
+// One body (gemm_body), four entry points: mpgemm_kernel (plain),
+// mpgemm_splitk_kernel (MPFK_FAST segments), mpgemm_pull_kernel (fused
+// all-gather, PullB) and mpgemm_gated_kernel (K panels flagged by the copy
+// engines, GateArgs).  The pull/gate bookkeeping is out of line so every
+// variant's main loop is the same instruction stream.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -46,7 +52,7 @@ struct GemmArgs {
   long long sa, sb, sc;
 };
 
-// Fused all-gather -> GEMM (mpgemm_kernel<Cfg, true>): B is not resident
+// Fused all-gather -> GEMM (mpgemm_pull_kernel, gemm_body mode 1): B is not resident
 // yet; its rows live in up to 8 source slices (other ranks' memory reached
 // over NVLink peer mappings, or local buffers when emulated on one GPU).
 // Before a CTA stages the k-tile of panel p it makes sure panel p has been
