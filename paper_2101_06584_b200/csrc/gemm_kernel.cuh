@@ -18,10 +18,10 @@
 // the 20-218 FP64 operations per multiply-add, so the kernel is bound by the
 // FP64 pipe, not by HBM, L2 or shared memory.
 //
-// One body (gemm_body), four entry points: mpgemm_kernel (plain),
-// mpgemm_splitk_kernel (MPFK_FAST segments), mpgemm_pull_kernel (fused
-// all-gather, PullB) and mpgemm_gated_kernel (K panels flagged by the copy
-// engines, GateArgs).  The pull/gate bookkeeping is out of line so every
+// One tile body (tile_run, called by gemm_body for one tile per CTA), four
+// entry points: mpgemm_kernel (plain), mpgemm_splitk_kernel (MPFK_FAST
+// segments), mpgemm_pull_kernel (fused all-gather, PullB) and
+// mpgemm_gated_kernel (K panels flagged by the copy engines, GateArgs).  The pull/gate bookkeeping is out of line so every
 // variant's main loop is the same instruction stream.
 #pragma once
 
@@ -283,12 +283,15 @@ __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W]
     }
 }
 
+// One output tile (rows m0.., columns n0..) over the K range of g: the
+// k = 0 step initialises the chains unless g.accumulate, which continues the
+// chains stored in C.
 // kMode: 0 plain, 1 fused all-gather (PullB), 2 copy-engine gated (GateArgs)
 template <class Cfg, int kMode>
-__device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, int klast = 0,
-                                          const GateArgs& G = GateArgs{}) {
+__device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, const PullB& P,
+                                         const GateArgs& G) {
   constexpr bool kPull = kMode == 1, kGate = kMode == 2;
-  constexpr int W = Cfg::W, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
+  constexpr int W = Cfg::W, BM = Cfg::BM, BK = Cfg::BK;
   constexpr int TM = Cfg::TM, TN = Cfg::TN, TX = Cfg::TX, TY = Cfg::TY;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ __align__(16) double smem[];
@@ -296,20 +299,6 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, in
   double* Bs0 = smem + STAGES * Cfg::A_STAGE;
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const int tiles_m = (g0.M + BM - 1) / BM, tiles_n = (g0.N + BN - 1) / BN;
-  int lin = blockIdx.x, bz = 0;
-  if (g0.batch > 1) {
-    bz = lin / (tiles_m * tiles_n);
-    lin -= bz * tiles_m * tiles_n;
-  }
-  GemmArgs g = g0;
-  if (klast && bz == g0.batch - 1) g.K = klast;  // split-K: ragged last segment
-  g.A += bz * g0.sa;
-  g.B += bz * g0.sb;
-  g.C += bz * g0.sc;
-  int tile_m, tile_n;
-  tile_coords<Cfg::GROUP_M>(lin, tiles_m, tiles_n, tile_m, tile_n);
-  const int m0 = tile_m * BM, n0 = tile_n * BN;
   const int ktiles = (g.K + BK - 1) / BK;
 
   double acc[TM][TN][W];
@@ -420,6 +409,26 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, in
       atomicAdd(G.band_done + m0 / G.band_rows, 1u);
     }
   }
+}
+
+// One CTA = one tile (blockIdx.x in GROUP_M order; batch-major for batches).
+template <class Cfg, int kMode>
+__device__ __forceinline__ void gemm_body(const GemmArgs& g0, const PullB& P, int klast = 0,
+                                          const GateArgs& G = GateArgs{}) {
+  const int tiles_m = (g0.M + Cfg::BM - 1) / Cfg::BM, tiles_n = (g0.N + Cfg::BN - 1) / Cfg::BN;
+  int lin = blockIdx.x, bz = 0;
+  if (g0.batch > 1) {
+    bz = lin / (tiles_m * tiles_n);
+    lin -= bz * tiles_m * tiles_n;
+  }
+  GemmArgs g = g0;
+  if (klast && bz == g0.batch - 1) g.K = klast;  // split-K: ragged last segment
+  g.A += bz * g0.sa;
+  g.B += bz * g0.sb;
+  g.C += bz * g0.sc;
+  int tile_m, tile_n;
+  tile_coords<Cfg::GROUP_M>(lin, tiles_m, tiles_n, tile_m, tile_n);
+  tile_run<Cfg, kMode>(g, tile_m * Cfg::BM, tile_n * Cfg::BN, P, G);
 }
 
 template <class Cfg>

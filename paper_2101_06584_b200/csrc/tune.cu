@@ -68,19 +68,290 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
 
 const Entry kEntries[] = {
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
-    E(2, 64, 64, 24, 4, 4, 2, 2, 16, 2),
-    E(2, 64, 64, 24, 4, 4, 2, 3, 16, 2),
-    E(2, 64, 64, 16, 4, 4, 2, 4, 16, 2),
-    E(2, 64, 64, 32, 4, 4, 2, 2, 16, 1),
-    E(2, 64, 64, 8, 4, 4, 3, 2, 16, 2),
+    E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // DD few-wave product
+    E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),  // TD product
+    E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),  // QD product
 };
+
+// Compute-only ceiling of a tile configuration: the product's mac_step on
+// one shared-memory stage filled once -- no global loads, no cp.async, no
+// barriers in the loop -- so the gap between this and the GEMM is what the
+// data movement and tile turnover cost, and the gap between this and the
+// DFMA-chain peak is what the DD/TD/QD instruction stream itself costs.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) ceiling_kernel(const double* src, double* out, int ktiles) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + Cfg::A_STAGE;
+  // component w of every operand is scaled by 2^(-55 w): renormalised
+  // multi-component values, so TD/QD take the GEMM's common renorm5 path
+  for (int i = threadIdx.x; i < Cfg::A_STAGE + Cfg::B_STAGE; i += Cfg::THREADS) {
+    const int w = i < Cfg::A_STAGE ? i / (Cfg::BM * Cfg::AS) : (i - Cfg::A_STAGE) / (Cfg::BK * Cfg::BS);
+    smem[i] = ldexp(src[(i * 7 + blockIdx.x) & 4095], -55 * w);
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % Cfg::TX, ty = threadIdx.x / Cfg::TX;
+  double acc[Cfg::TM][Cfg::TN][Cfg::W];
+#pragma unroll
+  for (int i = 0; i < Cfg::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::TN; ++j)
+#pragma unroll
+      for (int w = 0; w < Cfg::W; ++w) acc[i][j][w] = 0.0;
+  for (int kt = 0; kt < ktiles; ++kt) {
+#pragma unroll Cfg::KUNROLL
+    for (int q = 0; q < Cfg::BK; ++q) mac_step<Cfg>(acc, As, Bs, tx, ty, q);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < Cfg::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::TN; ++j) s += acc[i][j][0];
+  out[blockIdx.x * Cfg::THREADS + threadIdx.x] = s;
+}
+
+// EXPERIMENT (not in the product; profiles/r01_tune_persist.log):
+// Stream-K over chain continuation (mpgemm_streamk_kernel).  A persistent
+// grid of exactly the resident CTA slots (SMs x occupancy, so every SM holds
+// the same number of CTAs).  The first dp_waves waves run whole tiles
+// round-robin -- wave w gives CTA j tile w * gridDim.x + j, so the CTAs
+// resident at one time cover consecutive tiles of the GROUP_M raster, as in
+// the one-tile-per-CTA launch.  The k-tiles ("units") of the remaining
+// tiles are split evenly: CTA j owns units [U j / P, U (j+1) / P) of the
+// tile-major unit order.  There is no K reduction: a tile cut by a range
+// boundary is computed as a prefix (k-tiles [0, x), CTA j) and a suffix
+// ([x, kt), CTA j+1) that continues the chains the prefix stored in C --
+// the reference itself carries each chain in C between k steps
+// (linalg.hpp:261), so every element is bit-identical.  Each CTA runs its
+// prefix piece FIRST and its suffix piece LAST, so a suffix only ever waits
+// for work that started at the same time and depends on nothing; the host
+// guarantees U / P >= kt (a range spans at least one whole tile), so no tile
+// is cut twice.  Why: the hardware packs a partial last wave onto as few
+// SMs as it can, so the one-tile-per-CTA grid loses up to a wave (DD n=1024:
+// 1024 tiles on 592 slots ran at 0.86 of the steady rate).
+struct StreamK {
+  int* flags;    // [tiles - sk_first] prefix stored in C; zeroed before the launch
+  int dp_waves;  // whole-tile waves before the split region
+  int sk_first;  // first tile of the split region (dp_waves * gridDim.x)
+};
+
+__device__ __noinline__ void sk_wait(const int* f) {
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    while (ld_acquire_gpu(f) == 0) {
+      __nanosleep(128);
+      if (clock64() - t0 > (1ll << 37)) __trap();  // ~70 s: a lost prefix, fail loudly
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __noinline__ void sk_signal(int* f) {
+  __syncthreads();  // every thread's C stores of the prefix ...
+  if (threadIdx.x == 0) {
+    __threadfence();  // ... ordered before the flag (release)
+    atomicExch(f, 1);
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_streamk_kernel(const GemmArgs g, const StreamK sk) {
+  constexpr int BK = Cfg::BK;
+  const int tiles_m = (g.M + Cfg::BM - 1) / Cfg::BM, tiles_n = (g.N + Cfg::BN - 1) / Cfg::BN;
+  const int kt = (g.K + BK - 1) / BK;
+  // the CTA's segments, in order: dp_waves whole tiles; then, in the split
+  // region, the prefix of its last tile, its whole tiles, the suffix of its
+  // first tile (one loop, so the tile body is instantiated once)
+  const int P = (int)gridDim.x, j = (int)blockIdx.x;
+  const long long U = (long long)(tiles_m * tiles_n - sk.sk_first) * kt;
+  const long long beg = U * j / P, end = U * (j + 1) / P;
+  int t0 = 0, x = 0, t1 = -1, y = kt;
+  if (beg < end) {
+    t0 = (int)(beg / kt), x = (int)(beg % kt);
+    t1 = (int)((end - 1) / kt), y = (int)(end - (long long)t1 * kt);
+  }
+  const int has_pre = beg < end && y < kt, has_suf = beg < end && x > 0;
+  const int wfirst = has_suf ? t0 + 1 : t0, wlast = has_pre ? t1 - 1 : t1;
+  const int nwhole = beg < end ? max(0, wlast - wfirst + 1) : 0;
+  const int nseg = sk.dp_waves + has_pre + nwhole + has_suf;
+  for (int i = 0; i < nseg; ++i) {
+    int t, ka = 0, kb = kt, flag = -1, wait = 0;
+    if (i < sk.dp_waves) {
+      t = i * P + j;
+    } else {
+      int r = i - sk.dp_waves;
+      if (r < has_pre) {
+        t = t1, kb = y, flag = t1;  // prefix: publish when stored
+      } else if ((r -= has_pre) < nwhole) {
+        t = wfirst + r;
+      } else {
+        t = t0, ka = x, flag = t0, wait = 1;  // suffix: after its prefix
+      }
+      t += sk.sk_first;
+    }
+    if (wait) sk_wait(sk.flags + flag);
+    int tm, tn;
+    tile_coords<Cfg::GROUP_M>(t, tiles_m, tiles_n, tm, tn);
+    GemmArgs h = g;
+    h.A += (long long)ka * BK;
+    h.B += (long long)ka * BK * g.ldb;
+    h.K = min(g.K, kb * BK) - ka * BK;
+    h.accumulate = g.accumulate | (ka > 0);
+    tile_run<Cfg, 0>(h, tm * Cfg::BM, tn * Cfg::BN, PullB{}, GateArgs{});
+    if (flag >= 0 && !wait) sk_signal(sk.flags + flag);
+  }
+}
+
+// Persistent-grid experiments (grid = SMs x occupancy): round-robin whole
+// tiles, dynamic whole tiles (atomic tile counter), and the product stream-K
+// schedule, to compare with the one-tile-per-CTA launch.
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) persist_kernel(const GemmArgs g, int* counter) {
+  const int tiles_m = (g.M + Cfg::BM - 1) / Cfg::BM, tiles_n = (g.N + Cfg::BN - 1) / Cfg::BN;
+  const int tiles = tiles_m * tiles_n;
+  __shared__ int s_t;
+  for (int i = 0;; ++i) {
+    int t;
+    if (counter) {
+      __syncthreads();
+      if (threadIdx.x == 0) s_t = atomicAdd(counter, 1);
+      __syncthreads();
+      t = s_t;
+    } else {
+      t = i * (int)gridDim.x + (int)blockIdx.x;
+    }
+    if (t >= tiles) break;
+    int tm, tn;
+    tile_coords<Cfg::GROUP_M>(t, tiles_m, tiles_n, tm, tn);
+    tile_run<Cfg, 0>(g, tm * Cfg::BM, tn * Cfg::BN, PullB{}, GateArgs{});
+  }
+}
+
+template <class Cfg>
+int slots_of(const void* fn) {
+  int occ = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, Cfg::THREADS, Cfg::SMEM);
+  return occ * sms;
+}
+
+// mode 0: round-robin, 1: dynamic counter, 2: product stream-K
+template <class Cfg, int kMode>
+cudaError_t run_persist(const GemmArgs& g, cudaStream_t s) {
+  const long long tiles = (long long)((g.N + Cfg::BN - 1) / Cfg::BN) * ((g.M + Cfg::BM - 1) / Cfg::BM);
+  int* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(int) * (tiles + 1), s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(ws, 0, sizeof(int) * (tiles + 1), s);
+  if (kMode == 2) {
+    cudaFuncSetAttribute(mpgemm_streamk_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    const int P = slots_of<Cfg>((const void*)mpgemm_streamk_kernel<Cfg>);
+    StreamK sk;
+    sk.flags = ws;
+    sk.dp_waves = (int)(tiles / P) - 1;
+    sk.sk_first = sk.dp_waves * P;
+    if (tiles <= P || tiles % P == 0) sk.dp_waves = (int)((tiles + P - 1) / P), sk.sk_first = (int)tiles;
+    mpgemm_streamk_kernel<Cfg><<<P, Cfg::THREADS, Cfg::SMEM, s>>>(g, sk);
+  } else {
+    cudaFuncSetAttribute(persist_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    const int P = slots_of<Cfg>((const void*)persist_kernel<Cfg>);
+    persist_kernel<Cfg><<<P, Cfg::THREADS, Cfg::SMEM, s>>>(g, kMode == 1 ? ws : nullptr);
+  }
+  e = cudaGetLastError();
+  cudaFreeAsync(ws, s);
+  return e;
+}
+
+#define PE(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, MODE, TAG)                                        \
+  {W, TAG "/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB,   \
+   run_persist<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>, MODE>,                                \
+   info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
+
+const Entry kPersist[] = {
+    PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 0, "rr"),  PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 1, "dyn"),
+    PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 2, "sk"),  PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 0, "rr"),
+    PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 1, "dyn"), PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 2, "sk"),
+    PE(3, 32, 32, 16, 2, 2, 2, 1, 16, 3, 0, "rr"),  PE(3, 32, 32, 16, 2, 2, 2, 1, 16, 3, 1, "dyn"),
+    PE(3, 32, 32, 16, 2, 2, 2, 1, 16, 3, 2, "sk"),  PE(4, 16, 32, 16, 1, 2, 2, 1, 16, 3, 0, "rr"),
+    PE(4, 16, 32, 16, 1, 2, 2, 1, 16, 3, 1, "dyn"), PE(4, 16, 32, 16, 1, 2, 2, 1, 16, 3, 2, "sk"),
+};
+
+struct CEntry {
+  int W;
+  const char* name;
+  cudaError_t (*run)(const double*, double*, int, int, cudaStream_t);
+  long long macs_per_block_ktile;
+};
+
+template <class Cfg>
+cudaError_t run_ceiling(const double* src, double* out, int blocks, int ktiles, cudaStream_t s) {
+  const size_t sm = sizeof(double) * (Cfg::A_STAGE + Cfg::B_STAGE);
+  cudaError_t e = cudaFuncSetAttribute(ceiling_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  ceiling_kernel<Cfg><<<blocks, Cfg::THREADS, sm, s>>>(src, out, ktiles);
+  return cudaGetLastError();
+}
+
+#define CE(W, BM, BN, BK, TM, TN, ST, KU, GM, MB)                                                  \
+  {W, "ceiling/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/ku" #KU "/mb" #MB,                   \
+   run_ceiling<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>, (long long)BM * BN * BK}
+
+const CEntry kCeil[] = {
+    CE(2, 64, 64, 16, 4, 4, 2, 2, 16, 1),  // DD, one CTA per SM
+    CE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
+    CE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // DD few-wave
+    CE(2, 64, 32, 16, 4, 4, 2, 2, 16, 4),
+    CE(2, 32, 32, 8, 4, 4, 2, 2, 16, 8),
+    CE(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),  // TD product
+    CE(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),  // QD product
+};
+
+__global__ void pipe_peak_kernel(double* out, int iters, double m, int kind) {
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3 + j;
+  if (kind == 0) {
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = __fma_rn(a[j], m, 1e-9);
+  } else if (kind == 1) {
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = __dadd_rn(a[j], m);
+  } else {
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = __dmul_rn(a[j], m);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  if (s == 12345.678) out[0] = s;
+}
 }  // namespace
 
 extern "C" {
-int tune_count(void) { return (int)(sizeof(kEntries) / sizeof(kEntries[0])); }
-int tune_width(int i) { return kEntries[i].W; }
-const char* tune_name(int i) { return kEntries[i].name; }
-int tune_info(int i, int* regs, int* smem, int* threads) { return (int)kEntries[i].info(regs, smem, threads); }
+int ceil_count(void) { return (int)(sizeof(kCeil) / sizeof(kCeil[0])); }
+int ceil_width(int i) { return kCeil[i].W; }
+const char* ceil_name(int i) { return kCeil[i].name; }
+long long ceil_macs(int i) { return kCeil[i].macs_per_block_ktile; }
+int ceil_run(int i, const double* src, double* out, int blocks, int ktiles, void* stream) {
+  return (int)kCeil[i].run(src, out, blocks, ktiles, (cudaStream_t)stream);
+}
+// kind 0: DFMA chains, 1: DADD chains, 2: DMUL chains (8 per thread)
+int pipe_peak_run(int kind, double* out, int blocks, int threads, int iters, void* stream) {
+  pipe_peak_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(out, iters, kind == 1 ? 1e-300 : 0.999999, kind);
+  return (int)cudaGetLastError();
+}
+static const Entry& entry(int i) {
+  const int ne = (int)(sizeof(kEntries) / sizeof(kEntries[0]));
+  return i < ne ? kEntries[i] : kPersist[i - ne];
+}
+int tune_count(void) { return (int)(sizeof(kEntries) / sizeof(kEntries[0]) + sizeof(kPersist) / sizeof(kPersist[0])); }
+int tune_width(int i) { return entry(i).W; }
+const char* tune_name(int i) { return entry(i).name; }
+int tune_info(int i, int* regs, int* smem, int* threads) { return (int)entry(i).info(regs, smem, threads); }
 int tune_run(int i, int M, int N, int K, const double* A, long long lda, long long pa, const double* B,
              long long ldb, long long pb, double* C, long long ldc, long long pc, void* stream) {
   GemmArgs g;
@@ -89,6 +360,6 @@ int tune_run(int i, int M, int N, int K, const double* A, long long lda, long lo
   g.M = M, g.N = N, g.K = K;
   g.accumulate = 0;
   g.batch = 1, g.sa = g.sb = g.sc = 0;
-  return (int)kEntries[i].run(g, (cudaStream_t)stream);
+  return (int)entry(i).run(g, (cudaStream_t)stream);
 }
 }
