@@ -60,13 +60,60 @@ MPFK_HD double sel(bool p, double a, double b) { return p ? a : b; }
 // EFT primitives, eft.hpp:46-113.
 // ---------------------------------------------------------------------------
 
-// Knuth two-sum, eft.hpp:46-51 (6 ops).
-MPFK_HD void two_sum(double a, double b, double& s, double& e) {
+// Knuth two-sum, eft.hpp:46-51 (6 FP64 ops), literally.
+MPFK_HD void two_sum_knuth(double a, double b, double& s, double& e) {
   const double ss = add(a, b);
   const double v = sub(ss, a);
   e = add(sub(a, sub(ss, v)), sub(b, v));
   s = ss;
 }
+
+// Magnitude key: the high word without its sign bit, shifted up -- exponent
+// first, so key(x) >= key(y) implies exponent(x) >= exponent(y).
+#if defined(__CUDA_ARCH__)
+MPFK_HD uint32_t mag_key(double x) { return static_cast<uint32_t>(__double2hiint(x)) << 1; }
+#else
+MPFK_HD uint32_t mag_key(double x) {
+  uint64_t u;
+  std::memcpy(&u, &x, sizeof u);
+  return static_cast<uint32_t>(u >> 32) << 1;
+}
+#endif
+
+// The same (s, e) as two_sum_knuth with 3 FP64 ops: order the operands by
+// exponent on the integer pipes, then Dekker's fast two-sum.  Why it is
+// bit-identical for finite operands whose sum does not overflow:
+//  * s = a + b is the same rounded sum (x + y = a + b, commutative);
+//  * exponent(x) >= exponent(y) (Dekker's condition; equal exponents may go
+//    either way, subnormals included), so x - s = -(s - x) is exact and
+//    (x - s) + y = (a + b) - s is the exact rounding error, representable,
+//    hence computed exactly -- the same real number Knuth's form yields;
+//  * signed zeros: Knuth's e is never -0 (its last add is -0 only if both
+//    addends are -0, i.e. b = -0 with v = s - a = +0, but then a - (s - v)
+//    = +0).  (x - s) + y is -0 only if x - s = -0 and y = -0; x - s = -0
+//    needs x = -0 and s = +0, and then y = s - x... = +0.  So both give +0
+//    whenever the error is zero.
+// The sort costs one compare, two key shifts and four 32-bit selects on the
+// integer pipes.  MEASURED SLOWER on the B200 (profiles/r01_ceiling_two_sum.log):
+// the DD register-resident ceiling drops from 0.975 to 0.940 of the DFMA
+// peak (17 instead of 20 FP64 instructions per MAC, but the pipe then idles
+// ~20 %), TD 0.972 -> 0.890, QD 0.916 -> 0.844; the GEMMs lose 3-8 %.  So the
+// product keeps Knuth's form; this one is opt-in (-DMPFK_TWO_SUM_SORTED) and
+// stays bit-identical (tests/test_arith_host.py checks it against Knuth's
+// form on signed zeros, subnormals, ties and cancelling pairs).
+MPFK_HD void two_sum_sorted(double a, double b, double& s, double& e) {
+  const bool p = mag_key(a) >= mag_key(b);
+  const double x = sel(p, a, b), y = sel(p, b, a);
+  const double ss = add(a, b);
+  e = add(sub(x, ss), y);
+  s = ss;
+}
+
+#ifdef MPFK_TWO_SUM_SORTED
+MPFK_HD void two_sum(double a, double b, double& s, double& e) { two_sum_sorted(a, b, s, e); }
+#else
+MPFK_HD void two_sum(double a, double b, double& s, double& e) { two_sum_knuth(a, b, s, e); }
+#endif
 
 // Dekker fast-two-sum, eft.hpp:55-59 (3 ops).
 MPFK_HD void qts(double a, double b, double& s, double& e) {

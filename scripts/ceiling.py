@@ -16,7 +16,7 @@ import torch  # noqa: E402
 
 OPS = {2: 20, 3: 132, 4: 218}
 MINB = {"mb1": 1, "mb2": 2, "mb3": 3, "mb4": 4, "mb6": 6, "mb8": 8}
-T = C.CDLL(os.path.join(ROOT, "paper_2101_06584_b200", "libmpfk_tune.so"))
+T = C.CDLL(os.path.join(ROOT, "paper_2101_06584_b200", os.environ.get("TUNE_LIB", "libmpfk_tune.so")))
 T.ceil_name.restype = C.c_char_p
 T.ceil_macs.restype = C.c_longlong
 T.ceil_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]

@@ -76,4 +76,12 @@ void hst_gemm(int W, std::size_t m, std::size_t K, std::size_t n, const double* 
     }
 }
 
+// two_sum_sorted vs the literal Knuth form, pairwise
+void hst_two_sum_pair_batch(std::size_t count, const double* a, const double* b, double* out) {
+  for (std::size_t i = 0; i < count; ++i) {
+    two_sum_knuth(a[i], b[i], out[4 * i], out[4 * i + 1]);
+    two_sum_sorted(a[i], b[i], out[4 * i + 2], out[4 * i + 3]);
+  }
+}
+
 }  // extern "C"

@@ -165,3 +165,40 @@ def test_td_add_merge_host(H):
     want = np.empty_like(x)
     O.ref().ref_td_add_merge_batch(n, x.ctypes.data, y.ctypes.data, want.ctypes.data)
     assert not (r.view(np.uint64) != want.view(np.uint64)).any()
+
+
+def test_two_sum_sorted_equals_knuth(H):
+    """The 3-FP64-op two-sum (operands ordered by exponent on the integer
+    pipes, then Dekker's fast two-sum, mpf_arith.cuh:two_sum_sorted) returns
+    the same bits as Knuth's 6-op two_sum (eft.hpp:46-51) -- sum, error and
+    the sign of a zero error -- on signed zeros, subnormals, equal and
+    distant exponents, exact cancellation and random pairs."""
+    H.hst_two_sum_pair_batch.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(2101)
+    pool = np.array([0.0, -0.0, 1.0, -1.0, 0.5, -0.5, 1.5, 3.0, -3.0, 2.0 ** -53, -2.0 ** -53, 2.0 ** -1074,
+                     -2.0 ** -1074, 2.0 ** -1022, -2.0 ** -1022, 2.0 ** -1023, 1.0 + 2.0 ** -52, -(1.0 + 2.0 ** -52),
+                     2.0 ** 52, 2.0 ** 53 + 2, 2.0 ** 1000, -2.0 ** 1000, 2.0 ** -1000, np.nextafter(1.0, 0.0)])
+    n = 400_000
+    a = rng.choice(pool, n) * np.where(rng.integers(0, 2, n) == 1, 1.0, -1.0)
+    b = rng.choice(pool, n)
+    # random pairs: exponents near (cancellation), far, and subnormal
+    m = n // 4
+    r = rng.uniform(-1, 1, m)
+    a[:m] = r
+    b[:m] = -r * (1 + rng.integers(-8, 9, m) * 2.0 ** -52)
+    a[m:2 * m] = rng.uniform(-1, 1, m) * np.ldexp(1.0, rng.integers(-60, 61, m))
+    b[m:2 * m] = rng.uniform(-1, 1, m) * np.ldexp(1.0, rng.integers(-60, 61, m))
+    a[2 * m:2 * m + m // 2] = rng.integers(-2 ** 40, 2 ** 40, m // 2) * 2.0 ** -1074
+    b[2 * m:2 * m + m // 2] = rng.integers(-2 ** 40, 2 ** 40, m // 2) * 2.0 ** -1074
+    # same-magnitude pairs (key ties) in both orders
+    a[-1000:] = b[-1000:]
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    out = np.zeros((n, 4))
+    H.hst_two_sum_pair_batch(n, a.ctypes.data, b.ctypes.data, out.ctypes.data)
+    knuth = out[:, :2].view(np.uint64)
+    fast = out[:, 2:].view(np.uint64)
+    assert np.array_equal(knuth, fast), np.nonzero((knuth != fast).any(axis=1))[0][:10]
+    # and both orders of every pair
+    H.hst_two_sum_pair_batch(n, b.ctypes.data, a.ctypes.data, out.ctypes.data)
+    assert np.array_equal(out[:, :2].view(np.uint64), out[:, 2:].view(np.uint64))
