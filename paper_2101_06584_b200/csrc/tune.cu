@@ -6,6 +6,7 @@
 
 #include "gemm_kernel.cuh"
 #include "gemm_tma.cuh"
+#include "gemm_mbar.cuh"
 
 using namespace mpfk::kern;
 
@@ -263,12 +264,38 @@ cudaError_t run_persist(const GemmArgs& g, cudaStream_t s) {
   return e;
 }
 
+template <class Cfg>
+cudaError_t run_mbar_cfg(const GemmArgs& g, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(mpgemm_mbar_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Cfg::SMEM);
+  if (e != cudaSuccess) return e;
+  const long long tiles = (long long)((g.N + Cfg::BN - 1) / Cfg::BN) * ((g.M + Cfg::BM - 1) / Cfg::BM);
+  mpgemm_mbar_kernel<Cfg><<<(unsigned)tiles, Cfg::THREADS, Cfg::SMEM, s>>>(g);
+  return cudaGetLastError();
+}
+template <class Cfg>
+cudaError_t info_mbar_cfg(int* regs, int* smem, int* threads) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, mpgemm_mbar_kernel<Cfg>);
+  *regs = a.numRegs;
+  *smem = (int)Cfg::SMEM;
+  *threads = Cfg::THREADS;
+  return e;
+}
+#define MB(W, BM, BN, BK, TM, TN, ST, KU, GM, MB_)                                                  \
+  {W, "mbar/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB_,   \
+   run_mbar_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB_>>,                                   \
+   info_mbar_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB_>>}
+
 #define PE(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, MODE, TAG)                                        \
   {W, TAG "/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB,   \
    run_persist<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>, MODE>,                                \
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
 
 const Entry kPersist[] = {
+    MB(2, 64, 64, 16, 4, 4, 3, 2, 16, 2), MB(2, 64, 64, 8, 4, 4, 4, 2, 16, 2),
+    MB(3, 32, 32, 8, 2, 2, 4, 1, 16, 3),  MB(4, 16, 32, 8, 1, 2, 4, 1, 16, 3),
+    MB(2, 32, 32, 16, 2, 2, 3, 2, 16, 4),
     PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 0, "rr"),  PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 1, "dyn"),
     PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 2, "sk"),  PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 0, "rr"),
     PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 1, "dyn"), PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 2, "sk"),
