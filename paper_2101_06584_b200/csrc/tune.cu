@@ -28,6 +28,19 @@ cudaError_t run_cfg(const GemmArgs& g, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// one tile per CTA with extra dynamic shared memory: caps the CTAs per SM
+// (the hardware fills an SM before the next, so tiles = SMs x cap puts the
+// same number of tiles on every SM)
+template <class Cfg, int SMEM_KB>
+cudaError_t run_cfg_smem(const GemmArgs& g, cudaStream_t s) {
+  const int bytes = SMEM_KB * 1024 > (int)Cfg::SMEM ? SMEM_KB * 1024 : (int)Cfg::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(mpgemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  const long long tiles = (long long)((g.N + Cfg::BN - 1) / Cfg::BN) * ((g.M + Cfg::BM - 1) / Cfg::BM);
+  mpgemm_kernel<Cfg><<<(unsigned)tiles, Cfg::THREADS, bytes, s>>>(g);
+  return cudaGetLastError();
+}
+
 template <class Cfg>
 cudaError_t run_tma_cfg(const GemmArgs& g, cudaStream_t s) {
   return launch_tma<Cfg>(g, s);
@@ -62,6 +75,11 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    run_tma_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>,                                    \
    info_tma_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
 
+#define ES(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, KB)                                              \
+  {W, #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB "/smem" #KB "k", \
+   run_cfg_smem<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>, KB>,                                   \
+   info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
+
 #define F(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX)                                                \
   {W, #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB "/fixk" #FX,  \
    run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>,                                      \
@@ -70,6 +88,10 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
 const Entry kEntries[] = {
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
     E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // DD few-wave product
+    E(2, 32, 32, 8, 4, 4, 2, 2, 16, 8),
+    ES(2, 32, 32, 8, 4, 4, 2, 2, 16, 8, 30),   // 7 CTAs/SM: 1024 tiles on 148 SMs
+    ES(2, 32, 32, 8, 4, 4, 2, 2, 16, 8, 36),   // 6 CTAs/SM
+    ES(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 75),  // Cfg2s at 3 CTAs/SM
     E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),  // TD product
     E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),  // QD product
 };
@@ -127,9 +149,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) ceiling_kernel(const 
 // prefix piece FIRST and its suffix piece LAST, so a suffix only ever waits
 // for work that started at the same time and depends on nothing; the host
 // guarantees U / P >= kt (a range spans at least one whole tile), so no tile
-// is cut twice.  Why: the hardware packs a partial last wave onto as few
-// SMs as it can, so the one-tile-per-CTA grid loses up to a wave (DD n=1024:
-// 1024 tiles on 592 slots ran at 0.86 of the steady rate).
+// is cut twice.  (Measured slower than one tile per CTA: see DESIGN 4.2.)
 struct StreamK {
   int* flags;    // [tiles - sk_first] prefix stored in C; zeroed before the launch
   int dp_waves;  // whole-tile waves before the split region
@@ -206,12 +226,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) mpgemm_streamk_kernel
 // Persistent-grid experiments (grid = SMs x occupancy): round-robin whole
 // tiles, dynamic whole tiles (atomic tile counter), and the product stream-K
 // schedule, to compare with the one-tile-per-CTA launch.
+__device__ long long* g_trace = nullptr;  // [gridDim.x][4]: smid, start ns, end ns, tiles
+
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) persist_kernel(const GemmArgs g, int* counter) {
   const int tiles_m = (g.M + Cfg::BM - 1) / Cfg::BM, tiles_n = (g.N + Cfg::BN - 1) / Cfg::BN;
   const int tiles = tiles_m * tiles_n;
   __shared__ int s_t;
-  for (int i = 0;; ++i) {
+  long long t_start = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  int done = 0;
+  for (int i = 0;; ++i, ++done) {
     int t;
     if (counter) {
       __syncthreads();
@@ -225,6 +250,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) persist_kernel(const 
     int tm, tn;
     tile_coords<Cfg::GROUP_M>(t, tiles_m, tiles_n, tm, tn);
     tile_run<Cfg, 0>(g, tm * Cfg::BM, tn * Cfg::BN, PullB{}, GateArgs{});
+  }
+  if (threadIdx.x == 0 && g_trace) {
+    long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    long long* r = g_trace + 4 * blockIdx.x;
+    r[0] = sm, r[1] = t_start, r[2] = t_end, r[3] = done;
   }
 }
 
@@ -356,9 +389,39 @@ __global__ void pipe_peak_kernel(double* out, int iters, double m, int kind) {
   for (int j = 0; j < 8; ++j) s += a[j];
   if (s == 12345.678) out[0] = s;
 }
+
+// CTA placement probe: every CTA records the SM it runs on and the clock
+// when it started, then spins ~spin_ns so the grid's CTAs overlap.
+__global__ void smid_probe_kernel(int* smid, long long* start, long long spin_ns) {
+  extern __shared__ double pad[];
+  if (threadIdx.x == 0) {
+    unsigned s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    smid[blockIdx.x] = (int)s;
+    long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    start[blockIdx.x] = t0;
+    long long t = t0;
+    while (t - t0 < spin_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    pad[0] = (double)t;
+  }
+  __syncthreads();
+}
 }  // namespace
 
 extern "C" {
+int persist_trace(long long* buf) {  // device buffer of 4 x grid long longs, or NULL
+  return (int)cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf));
+}
+int smid_probe(int blocks, int threads, int smem_bytes, long long spin_ns, int* smid, long long* start,
+               void* stream) {
+  cudaError_t e = cudaFuncSetAttribute(smid_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_bytes > 0 ? smem_bytes : 0);
+  if (e != cudaSuccess) return (int)e;
+  smid_probe_kernel<<<blocks, threads, smem_bytes > 8 ? smem_bytes : 8, (cudaStream_t)stream>>>(smid, start,
+                                                                                              spin_ns);
+  return (int)cudaGetLastError();
+}
 int ceil_count(void) { return (int)(sizeof(kCeil) / sizeof(kCeil[0])); }
 int ceil_width(int i) { return kCeil[i].W; }
 const char* ceil_name(int i) { return kCeil[i].name; }
