@@ -90,11 +90,15 @@ __device__ __forceinline__ void cp_async_wait() {
 // and share their A and B panels in L2 instead of streaming all of B per
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
-          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0>
+          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0>
 struct TileCfg {
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
   static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
   static constexpr int FIXK = FIXK_;  // full k-tiles run a constant-trip loop
+  // one __syncthreads per k-tile: wait for tile kt, barrier, THEN refill the
+  // slot of tile kt-1 (every warp is past it) and compute -- instead of
+  // refill, wait, barrier, compute, barrier
+  static constexpr int ONEBAR = ONEBAR_;
   static constexpr int TX = BN / TN;  // threads along N
   static constexpr int TY = BM / TM;  // threads along M
   static constexpr int THREADS = TX * TY;
@@ -335,6 +339,10 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
   }
 
   for (int kt = 0; kt < ktiles; ++kt) {
+    if (Cfg::ONEBAR) {
+      cp_async_wait<STAGES - 2>();  // tile kt has landed (later ones may be in flight)
+      __syncthreads();              // ... for every thread; every warp is done with kt-1
+    }
     // issue the tile STAGES-1 ahead into the slot freed last iteration
     {
       const int nt = kt + STAGES - 1;
@@ -353,8 +361,10 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
       }
       cp_async_commit();
     }
-    cp_async_wait<STAGES - 1>();
-    __syncthreads();
+    if (!Cfg::ONEBAR) {
+      cp_async_wait<STAGES - 1>();
+      __syncthreads();
+    }
 
     const int slot = kt % STAGES;
     const double* As = As0 + slot * Cfg::A_STAGE;
@@ -385,9 +395,10 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
 #pragma unroll Cfg::KUNROLL
       for (; kk < kend; ++kk) mac_step<Cfg>(acc, As, Bs, tx, ty, kk);
     }
-    __syncthreads();
+    if (!Cfg::ONEBAR) __syncthreads();
   }
   cp_async_wait<0>();
+  if (Cfg::ONEBAR) __syncthreads();  // the slots are free again (a persistent caller may refill them)
 
   if (ktiles == 0) return;  // K == 0 is handled by the host (C = +0)
 #pragma unroll

@@ -80,6 +80,11 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    run_cfg_smem<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>, KB>,                                   \
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
 
+#define E1(W, BM, BN, BK, TM, TN, ST, KU, GM, MB)                                                  \
+  {W, "onebar/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB,   \
+   run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 1>>,                                   \
+   info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 1>>}
+
 #define F(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX)                                                \
   {W, #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB "/fixk" #FX,  \
    run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>,                                      \
@@ -88,10 +93,11 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
 const Entry kEntries[] = {
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
     E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // DD few-wave product
-    E(2, 32, 32, 8, 4, 4, 2, 2, 16, 8),
-    ES(2, 32, 32, 8, 4, 4, 2, 2, 16, 8, 30),   // 7 CTAs/SM: 1024 tiles on 148 SMs
-    ES(2, 32, 32, 8, 4, 4, 2, 2, 16, 8, 36),   // 6 CTAs/SM
-    ES(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 75),  // Cfg2s at 3 CTAs/SM
+    E1(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // one barrier per k-tile
+    E1(2, 64, 64, 16, 4, 4, 3, 2, 16, 2),
+    E1(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),
+    E1(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),
+    E1(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),
     E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),  // TD product
     E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),  // QD product
 };
@@ -326,9 +332,6 @@ cudaError_t info_mbar_cfg(int* regs, int* smem, int* threads) {
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB>>}
 
 const Entry kPersist[] = {
-    MB(2, 64, 64, 16, 4, 4, 3, 2, 16, 2), MB(2, 64, 64, 8, 4, 4, 4, 2, 16, 2),
-    MB(3, 32, 32, 8, 2, 2, 4, 1, 16, 3),  MB(4, 16, 32, 8, 1, 2, 4, 1, 16, 3),
-    MB(2, 32, 32, 16, 2, 2, 3, 2, 16, 4),
     PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 0, "rr"),  PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 1, "dyn"),
     PE(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 2, "sk"),  PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 0, "rr"),
     PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 1, "dyn"), PE(2, 32, 32, 16, 2, 2, 2, 2, 16, 4, 2, "sk"),

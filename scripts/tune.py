@@ -4,6 +4,7 @@ BASELINE inputs; each result must be bit-identical to the product kernel's.
 import argparse
 import ctypes as C
 import json
+import re
 import os
 import sys
 
@@ -19,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", default="1024,4096")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--widths", default="2,3,4")
+ap.add_argument("--match", default="", help="regex: only entries whose name matches")
 a = ap.parse_args()
 
 T = C.CDLL(os.path.join(ROOT, "paper_2101_06584_b200", "libmpfk_tune.so"))
@@ -50,6 +52,8 @@ for W in [int(x) for x in a.widths.split(",")]:
             if T.tune_width(i) != W:
                 continue
             name = T.tune_name(i).decode()
+            if a.match and not re.search(a.match, name):
+                continue
             regs, smem, thr = C.c_int(), C.c_int(), C.c_int()
             T.tune_info(i, C.byref(regs), C.byref(smem), C.byref(thr))
             Cm = torch.zeros_like(A)
