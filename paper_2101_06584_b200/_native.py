@@ -78,6 +78,7 @@ _SIGS = {
     "mpfk_gemm_device_ex": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                       _U64, C.c_uint, _P, C.POINTER(C.c_int)]),
     "mpfk_splitk_segments": (C.c_int, [C.c_int, _U64, _U64, _U64]),
+    "mpfk_gemm_redo_count": (C.c_int, [C.POINTER(_U64), C.c_int]),
     "mpfk_ew_apply_into": (C.c_int, [C.c_int, C.c_int, C.POINTER(MpfkMat), C.POINTER(MpfkMat),
                                      C.POINTER(MpfkMat), C.c_int]),
     "mpfk_ew_device": (C.c_int, [C.c_int, C.c_int, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64,

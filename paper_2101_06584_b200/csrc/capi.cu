@@ -299,8 +299,11 @@ void grow(double*& p, size_t& cap, size_t bytes) {
 // most -- it caps registers so 2-3 CTAs share each SM's FP64 pipe.
 using Cfg2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 2, 16, 2>;     // DD, large problems
 using Cfg2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 2, 16, 4>;    // DD, few waves
-using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 3>;     // TD
-using Cfg4 = kern::TileCfg<4, 16, 32, 16, 1, 2, 2, 1, 16, 3>;     // QD
+// TD / QD: branch-free renorm5 in the k loop with an exact warp-level redo
+// of any k-tile that met a zero-residual input (TileCfg::FASTR,
+// profiles/r01_tune_fastr.log: QD n=4096 0.9225 -> 0.930, TD n=1024 +2.5 %).
+using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1>;  // TD
+using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1>;  // QD
 
 template <class Cfg>
 void configure_once() {
@@ -1539,6 +1542,21 @@ void mpfk_op_counters_read(uint64_t* adds, uint64_t* muls, uint64_t* leaf) {
   if (adds) *adds = g_adds.load(std::memory_order_relaxed);
   if (muls) *muls = g_muls.load(std::memory_order_relaxed);
   if (leaf) *leaf = g_leaf.load(std::memory_order_relaxed);
+}
+
+int mpfk_gemm_redo_count(uint64_t* count, int reset) {
+  return guarded([&] {
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    unsigned long long v = 0;
+    ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    ck(cudaMemcpyFromSymbol(&v, kern::g_fastr_redo, sizeof v), "cudaMemcpyFromSymbol");
+    if (count) *count = v;
+    if (reset) {
+      v = 0;
+      ck(cudaMemcpyToSymbol(kern::g_fastr_redo, &v, sizeof v), "cudaMemcpyToSymbol");
+    }
+  });
 }
 
 void* mpfk_host_alloc(uint64_t bytes) {

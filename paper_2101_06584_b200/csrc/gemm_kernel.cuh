@@ -74,6 +74,10 @@ struct PullB {
   int* done;               // [panels] chunks copied and published
 };
 
+// warp k-tiles recomputed with the exact renormalisation (TileCfg::FASTR);
+// read through mpfk_gemm_redo_count
+__device__ unsigned long long g_fastr_redo = 0;
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const int n = valid ? 16 : 0;  // src-size 0 -> 16 zero bytes, no global read
@@ -90,7 +94,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // and share their A and B panels in L2 instead of streaming all of B per
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
-          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0>
+          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0>
 struct TileCfg {
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
   static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
@@ -102,12 +106,19 @@ struct TileCfg {
   static constexpr int TX = BN / TN;  // threads along N
   static constexpr int TY = BM / TM;  // threads along M
   static constexpr int THREADS = TX * TY;
+  // TD/QD: run each k-tile with the branch-free renorm5 (paths A/B) and a
+  // per-thread "rare" flag; a warp that saw any input needing paths C/D
+  // restores its chains from a shared-memory snapshot taken at the k-tile
+  // start and recomputes the k-tile with the exact form (same smem stage,
+  // same order): bit-identical, and the common path has no branch
+  static constexpr int FASTR = (W_ >= 3) ? FASTR_ : 0;
+  static constexpr int SNAP = FASTR ? THREADS * TM * TN * W : 0;  // doubles
   static constexpr int APAD = 2, BPAD = 2;  // keep 16 B row alignment, spread banks
   static constexpr int AS = BK + APAD;      // A tile row stride (doubles), [BM][AS]
   static constexpr int BS = BN + BPAD;      // B tile row stride, [BK][BS]
   static constexpr int A_STAGE = W * BM * AS;
   static constexpr int B_STAGE = W * BK * BS;
-  static constexpr size_t SMEM = sizeof(double) * size_t(STAGES) * (A_STAGE + B_STAGE);
+  static constexpr size_t SMEM = sizeof(double) * (size_t(STAGES) * (A_STAGE + B_STAGE) + SNAP);
   static_assert(BK % 2 == 0 && BN % 2 == 0, "16-byte chunks");
   static_assert(BM % TM == 0 && BN % TN == 0, "micro-tile");
 };
@@ -287,6 +298,32 @@ __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W]
     }
 }
 
+// mac_step with the branch-free renormalisation (Cfg::FASTR); ORs into
+// `rare` when an input needed renorm5 paths C/D
+template <class Cfg>
+__device__ __forceinline__ void mac_step_fast(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W], const double* As,
+                                              const double* Bs, int tx, int ty, int kk, bool& rare) {
+  constexpr int W = Cfg::W, BM = Cfg::BM, BK = Cfg::BK, TM = Cfg::TM, TN = Cfg::TN;
+  constexpr int TX = Cfg::TX, TY = Cfg::TY;
+  double a[TM][W], b[TN][W];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
+#pragma unroll
+  for (int j = 0; j < TN; ++j)
+#pragma unroll
+    for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + kk * Cfg::BS + tx + j * TX];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      double p[W];
+      arith::mp_mul_f<W, true>(a[i], b[j], p, rare);
+      arith::mp_add_f<W, true>(acc[i][j], p, acc[i][j], rare);
+    }
+}
+
 // One output tile (rows m0.., columns n0..) over the K range of g: the
 // k = 0 step initialises the chains unless g.accumulate, which continues the
 // chains stored in C.
@@ -388,7 +425,28 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
         for (int j = 0; j < TN; ++j) arith::mp_mul<W>(a[i], b[j], acc[i][j]);
       kk = 1;
     }
-    if (Cfg::FIXK && kk == 0 && kend == BK) {
+    if constexpr (Cfg::FASTR) {
+      double* snap = smem + STAGES * (Cfg::A_STAGE + Cfg::B_STAGE) + threadIdx.x;
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int w = 0; w < W; ++w) snap[((i * TN + j) * W + w) * Cfg::THREADS] = acc[i][j][w];
+      bool rare = false;
+#pragma unroll Cfg::KUNROLL
+      for (int q = kk; q < kend; ++q) mac_step_fast<Cfg>(acc, As, Bs, tx, ty, q, rare);
+      if (__any_sync(0xffffffffu, rare)) {  // rare: this warp redoes the k-tile exactly
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_fastr_redo, 1ull);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[i][j][w] = snap[((i * TN + j) * W + w) * Cfg::THREADS];
+        for (int q = kk; q < kend; ++q) mac_step<Cfg>(acc, As, Bs, tx, ty, q);
+      }
+    } else if (Cfg::FIXK && kk == 0 && kend == BK) {
 #pragma unroll Cfg::KUNROLL
       for (int q = 0; q < BK; ++q) mac_step<Cfg>(acc, As, Bs, tx, ty, q);
     } else {

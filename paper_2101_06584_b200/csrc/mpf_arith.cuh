@@ -161,8 +161,16 @@ MPFK_HD void three_sum2(double a, double b, double c, double& s, double& e) {
 // Signed zeros: every slot the reference leaves untouched keeps its exact
 // value, including the +0 initialisers of s2/s3 (eft.hpp:251).
 // ---------------------------------------------------------------------------
-MPFK_HD void renorm5(double c0, double c1, double c2, double c3, double c4, double& r0,
-                     double& r1, double& r2, double& r3) {
+//
+// kFast: paths A/B only, branch-free, and `rare` is set when the input needs
+// paths C/D (a zero residual in the first two forward steps) -- the result
+// is then NOT the reference's, and the caller must recompute with the exact
+// form (gemm_kernel.cuh: a warp redoes its k-tile from a snapshot of C).
+// Without the branch the compiler interleaves a thread's independent chains
+// across the renormalisation (TD/QD GEMM +2-3 %).
+template <bool kFast>
+MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, double& r0,
+                       double& r1, double& r2, double& r3, bool& rare) {
   double t;
   qts(c3, c4, t, c4);
   qts(c2, t, t, c3);
@@ -172,7 +180,9 @@ MPFK_HD void renorm5(double c0, double c1, double c2, double c3, double c4, doub
   double s0, s1, u, s2;
   qts(c0, c1, s0, s1);
   qts(s1, c2, u, s2);
-  if (nz(s1) & nz(s2)) {
+  const bool ab = nz(s1) & nz(s2);
+  if (kFast) rare |= !ab;
+  if (kFast || ab) {
     // path A (s3 != 0: s3 += c4) or path B (s3 == 0: s2 += c4), eft.hpp:255-260
     double v, s3;
     qts(s2, c3, v, s3);
@@ -217,6 +227,12 @@ MPFK_HD void renorm5(double c0, double c1, double c2, double c3, double c4, doub
   r0 = s0, r1 = s1, r2 = s2, r3 = s3;
 }
 
+MPFK_HD void renorm5(double c0, double c1, double c2, double c3, double c4, double& r0,
+                     double& r1, double& r2, double& r3) {
+  bool rare = false;
+  renorm5_t<false>(c0, c1, c2, c3, c4, r0, r1, r2, r3, rare);
+}
+
 // vseb with k = 2 output slots over n = 3 inputs (the only use on the path:
 // td_mul, mpf.hpp:162), eft.hpp:205-225 unrolled:
 //   (a, r) = qts(e1, e2); eps = r != 0 ? r : a; (b, r2) = qts(eps, e3)
@@ -257,8 +273,8 @@ MPFK_HD void dd_mul(const double* x, const double* y, double* r) {
 // qd_add, mpf.hpp:178-196 (63 ops + renorm5).  With Trunc3 the fourth
 // output is not produced (td_add_q drops it, mpf.hpp:141), which lets the
 // compiler delete the dead tail of renorm5.
-template <bool Trunc3 = false>
-MPFK_HD void qd_add(const double* x, const double* y, double* r) {
+template <bool Trunc3 = false, bool kFast = false>
+MPFK_HD void qd_add(const double* x, const double* y, double* r, bool& rare) {
   double s0, t0, s1, t1, s2, t2, s3, t3;
   two_sum(x[0], y[0], s0, t0);
   two_sum(x[1], y[1], s1, t1);
@@ -269,13 +285,19 @@ MPFK_HD void qd_add(const double* x, const double* y, double* r) {
   three_sum2(s3, t0, t2, s3, t0);
   t0 = add(add(t0, t1), t3);
   double r3;
-  renorm5(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3);
+  renorm5_t<kFast>(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3, rare);
   if (!Trunc3) r[3] = r3;
+}
+template <bool Trunc3 = false>
+MPFK_HD void qd_add(const double* x, const double* y, double* r) {
+  bool rare = false;
+  qd_add<Trunc3, false>(x, y, r, rare);
 }
 
 // qd_mul, mpf.hpp:198-238 (111 ops + renorm5), including the pre-combined
 // operand pairs that keep it bitwise commutative (mpf.hpp:214-221).
-MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
+template <bool kFast>
+MPFK_HD void qd_mul_t(const double* x, const double* y, double* r, bool& rare) {
   double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
   two_prod(x[0], y[0], p0, q0);
   two_prod(x[0], y[1], p1, q1);
@@ -303,7 +325,11 @@ MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
   s1 = add(s1, q0);
   s1 = add(s1, add(q3, q5));
   s1 = add(s1, q4);
-  renorm5(p0, p1, s0, s1, s2, r[0], r[1], r[2], r[3]);
+  renorm5_t<kFast>(p0, p1, s0, s1, s2, r[0], r[1], r[2], r[3], rare);
+}
+MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
+  bool rare = false;
+  qd_mul_t<false>(x, y, r, rare);
 }
 
 // td_add_q, mpf.hpp:135-142: zero-extend with +0, quad add, truncate.
@@ -321,7 +347,8 @@ MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
 //  * t0 + t3 with t3 = +0 stays (same reason).
 // 11 of td_add_q's 85 FP64 operations disappear; results are unchanged
 // (tests/test_arith_host.py sweeps signed zeros against the reference).
-MPFK_HD void td_add_q(const double* x, const double* y, double* r) {
+template <bool kFast>
+MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, bool& rare) {
   double s0, t0, s1, t1, s2, t2;
   two_sum(x[0], y[0], s0, t0);
   two_sum(x[1], y[1], s1, t1);
@@ -335,7 +362,11 @@ MPFK_HD void td_add_q(const double* x, const double* y, double* r) {
   t0 = add(0.0, ue);
   t0 = add(add(t0, t1), 0.0);
   double r3;
-  renorm5(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3);
+  renorm5_t<kFast>(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3, rare);
+}
+MPFK_HD void td_add_q(const double* x, const double* y, double* r) {
+  bool rare = false;
+  td_add_q_t<false>(x, y, r, rare);
 }
 
 // td_add_q without the folds (the literal zero-extend + qd_add); kept for
@@ -444,6 +475,23 @@ MPFK_HD void td_mul_q(const double* x, const double* y, double* r) {
 }
 
 // Library width defaults, mpf.hpp:242-260.
+// kFast (GEMM inner loop): renorm5 paths A/B only; `rare` reports an input
+// that needed paths C/D (the result must then be recomputed exactly).  DD
+// has no data-dependent branch, so its kFast form is the exact one.
+template <int W, bool kFast>
+MPFK_HD void mp_add_f(const double* x, const double* y, double* r, bool& rare) {
+  if constexpr (W == 2) dd_add(x, y, r);
+  else if constexpr (W == 3) td_add_q_t<kFast>(x, y, r, rare);
+  else qd_add<false, kFast>(x, y, r, rare);
+}
+
+template <int W, bool kFast>
+MPFK_HD void mp_mul_f(const double* x, const double* y, double* r, bool& rare) {
+  if constexpr (W == 2) dd_mul(x, y, r);
+  else if constexpr (W == 3) td_mul(x, y, r);
+  else qd_mul_t<kFast>(x, y, r, rare);
+}
+
 template <int W>
 MPFK_HD void mp_add(const double* x, const double* y, double* r) {
   if constexpr (W == 2) dd_add(x, y, r);

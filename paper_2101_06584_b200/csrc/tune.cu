@@ -85,6 +85,11 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 1>>,                                   \
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 1>>}
 
+#define EF(W, BM, BN, BK, TM, TN, ST, KU, GM, MB)                                                  \
+  {W, "fastr/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB,    \
+   run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 0, 1>>,                                 \
+   info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 0, 1>>}
+
 #define F(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX)                                                \
   {W, #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB "/fixk" #FX,  \
    run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>,                                      \
@@ -93,11 +98,12 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
 const Entry kEntries[] = {
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
     E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // DD few-wave product
-    E1(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // one barrier per k-tile
-    E1(2, 64, 64, 16, 4, 4, 3, 2, 16, 2),
-    E1(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),
-    E1(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),
-    E1(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),
+    EF(3, 32, 32, 8, 2, 2, 2, 1, 16, 3),   // branch-free renorm5 + warp redo
+    EF(3, 32, 32, 16, 2, 2, 2, 1, 16, 2),
+    EF(3, 16, 32, 16, 1, 2, 2, 1, 16, 3),
+    EF(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),
+    EF(4, 16, 32, 8, 1, 2, 2, 1, 16, 3),
+    EF(4, 32, 32, 16, 2, 2, 2, 1, 16, 2),
     E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),  // TD product
     E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),  // QD product
 };

@@ -213,6 +213,14 @@ def splitk_segments(W: int, m: int, n: int, k: int) -> int:
     return r
 
 
+def gemm_redo_count(reset: bool = False) -> int:
+    """Warp k-tiles the TD/QD GEMM recomputed with the exact renorm5 paths
+    C/D on the current device since the last reset (mpfk_gemm_redo_count)."""
+    v = C.c_uint64(0)
+    N.check(N.lib().mpfk_gemm_redo_count(C.byref(v), 1 if reset else 0))
+    return v.value
+
+
 def matmul_block_parallel(A: MPMatrix, B: MPMatrix, n_min: int = 32,
                           variant: KernelVariant = KernelVariant.NORMAL, workers: int = 1,
                           pinned: bool = False) -> MPMatrix:

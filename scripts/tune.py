@@ -23,7 +23,7 @@ ap.add_argument("--widths", default="2,3,4")
 ap.add_argument("--match", default="", help="regex: only entries whose name matches")
 a = ap.parse_args()
 
-T = C.CDLL(os.path.join(ROOT, "paper_2101_06584_b200", "libmpfk_tune.so"))
+T = C.CDLL(os.path.join(ROOT, "paper_2101_06584_b200", os.environ.get("TUNE_LIB", "libmpfk_tune.so")))
 T.tune_name.restype = C.c_char_p
 T.tune_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p,
                        C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p]
