@@ -259,6 +259,11 @@ struct GateArgs {
   unsigned* band_done;
   int panel_rows;  // multiple of BK
   int band_rows;   // multiple of BM
+  // flags[p] covers B's panel p and A's panel p for rows < a_rows_first
+  // only (the rows the first wave of tiles computes, uploaded first); the
+  // remaining rows of A arrive after all panels and raise *a_rest
+  int a_rows_first;
+  const unsigned* a_rest;
 };
 
 // out of line: the main loop keeps the plain kernel's code generation
@@ -356,6 +361,7 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
   }
 
   int ready_panel = -1;  // kPull: panels [0, ready_panel] are resident (visited in order)
+  if (kGate && min(m0 + BM, g.M) > G.a_rows_first) wait_flag(G.a_rest);  // rows uploaded after the panels
 
   // prologue: fill STAGES-1 stages
 #pragma unroll

@@ -7,26 +7,46 @@
 // in about two first-wave durations (measured: DD/TD/QD n=1024, TD/QD n=4096
 // gain; DD n=8192 -- 2 GiB of operands against an 11 ms first wave -- keeps
 // the row-chunked path, whose chunk-0 GEMM walks B panel by panel).
-bool gate_pays(int W, uint64_t m, uint64_t n, uint64_t K, double upload_bw) {
+// The tile shape and occupancy the gated launch uses, and the rows of A the
+// first wave of tiles covers (whole GROUP_M bands of the tile raster,
+// gemm_kernel.cuh:tile_coords): those rows go up with B's panels, the rest
+// of A after them.
+struct GatePlan {
+  int bm, bn, minb;
+  uint64_t a_rows_first;
+  double waves;
+};
+GatePlan gate_plan(int W, uint64_t m, uint64_t n) {
   kern::GemmArgs g;
   g.M = (int)std::min<uint64_t>(m, 0x7fffffff), g.N = (int)std::min<uint64_t>(n, 0x7fffffff), g.batch = 1;
-  int BM = Cfg3::BM, BN = Cfg3::BN, minb = Cfg3::MINB;
-  if (W == 4) BM = Cfg4::BM, BN = Cfg4::BN, minb = Cfg4::MINB;
+  GatePlan p{Cfg3::BM, Cfg3::BN, Cfg3::MINB, 0, 1.0};
+  if (W == 4) p.bm = Cfg4::BM, p.bn = Cfg4::BN, p.minb = Cfg4::MINB;
   if (W == 2) {
     if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
-      BM = Cfg2s::BM, BN = Cfg2s::BN, minb = Cfg2s::MINB;
+      p.bm = Cfg2s::BM, p.bn = Cfg2s::BN, p.minb = Cfg2s::MINB;
     else
-      BM = Cfg2::BM, BN = Cfg2::BN, minb = Cfg2::MINB;
+      p.bm = Cfg2::BM, p.bn = Cfg2::BN, p.minb = Cfg2::MINB;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const double tiles = double((m + BM - 1) / BM) * double((n + BN - 1) / BN);
-  const double waves = std::max(1.0, tiles / (double(sms) * minb));
+  const double tiles_n = double((n + p.bn - 1) / p.bn);
+  const double tiles = double((m + p.bm - 1) / p.bm) * tiles_n;
+  const double slots = double(sms) * p.minb;
+  p.waves = std::max(1.0, tiles / slots);
+  constexpr int kGroupM = 16;  // TileCfg GROUP_M of every product configuration
+  const double bands = std::ceil(std::min(slots, tiles) / (kGroupM * tiles_n));
+  p.a_rows_first = std::min<uint64_t>(m, (uint64_t)bands * kGroupM * p.bm);
+  return p;
+}
+
+bool gate_pays(int W, uint64_t m, uint64_t n, uint64_t K, double upload_bw) {
+  const GatePlan p = gate_plan(W, m, n);
   const double ops = W == 2 ? 20.0 : W == 3 ? 132.0 : 218.0;
-  const double kern_s = double(m) * n * K * ops / 18e12;                   // ~FP64 peak
-  const double upload_s = 8.0 * W * (double(m) * K + double(K) * n) / upload_bw;
-  return upload_s <= 2.0 * kern_s / waves;
+  const double kern_s = double(m) * n * K * ops / 18e12;  // ~FP64 peak
+  // what the first wave waits for: B and the first-wave rows of A
+  const double upload_s = 8.0 * W * (double(p.a_rows_first) * K + double(K) * n) / upload_bw;
+  return upload_s <= 2.0 * kern_s / p.waves;
 }
 
 // One GPU: ONE GEMM launch gated by the copy engines.  A and B are uploaded
@@ -55,7 +75,7 @@ void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, D
   const uint64_t npan = (K + pk - 1) / pk;
   const uint64_t band_rows = 256;  // a multiple of every configuration's BM
   const uint64_t nb = (m + band_rows - 1) / band_rows;
-  const size_t gate_bytes = sizeof(unsigned) * (npan + nb);
+  const size_t gate_bytes = sizeof(unsigned) * (npan + 1 + nb);
   if (gate_bytes > D.gate_cap) {
     if (D.gate) cudaFree(D.gate);
     D.gate = nullptr;
@@ -63,8 +83,10 @@ void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, D
     ck(cudaMalloc(reinterpret_cast<void**>(&D.gate), gate_bytes), "cudaMalloc(gate)");
     D.gate_cap = gate_bytes;
   }
-  unsigned* flags = D.gate;
-  unsigned* band_done = D.gate + npan;
+  unsigned* flags = D.gate;               // [npan] B panel + first-wave rows of A
+  unsigned* a_rest = D.gate + npan;       // the other rows of A
+  unsigned* band_done = D.gate + npan + 1;
+  const uint64_t m1 = gate_plan(W, m, n).a_rows_first;
 
   D.stage.reset();
   ck(cudaEventRecord(D.ev[0], D.up), "event");
@@ -83,20 +105,26 @@ void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, D
   g.M = (int)m, g.N = (int)n, g.K = (int)K;
   g.accumulate = 0;
   g.batch = 1, g.sa = g.sb = g.sc = 0;
-  kern::GateArgs gate{flags, band_done, (int)pk, (int)band_rows};
+  kern::GateArgs gate{flags, band_done, (int)pk, (int)band_rows, (int)m1, a_rest};
   const auto tile = dispatch_gemm_gated(W, g, gate, D.stream);
   ck(cudaEventRecord(D.ev[3], D.stream), "event");
 
   for (uint64_t p = 0; p < npan; ++p) {
     const uint64_t k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
     for (int w = 0; w < W; ++w) {
-      copy_h2d(D, a_pin, D.dA + w * m * lda + k0, lda, A->base + w * pa_h + k0, A->stride, k1 - k0, m, D.up);
+      copy_h2d(D, a_pin, D.dA + w * m * lda + k0, lda, A->base + w * pa_h + k0, A->stride, k1 - k0, m1, D.up);
       copy_h2d(D, b_pin, D.dB + w * K * ldb + k0 * ldb, ldb, B->base + w * pb_h + k0 * B->stride, B->stride, n,
                k1 - k0, D.up);
     }
     cu_ck(g_write32(reinterpret_cast<CUstream>(D.up), reinterpret_cast<CUdeviceptr>(flags + p), 1, 0),
           "cuStreamWriteValue32");
   }
+  if (m1 < m)
+    for (int w = 0; w < W; ++w)
+      copy_h2d(D, a_pin, D.dA + w * m * lda + m1 * lda, lda, A->base + w * pa_h + m1 * A->stride, A->stride, K,
+               m - m1, D.up);
+  cu_ck(g_write32(reinterpret_cast<CUstream>(D.up), reinterpret_cast<CUdeviceptr>(a_rest), 1, 0),
+        "cuStreamWriteValue32");
   ck(cudaEventRecord(D.ev[1], D.up), "event");
 
   ck(cudaStreamWaitEvent(D.down, D.ev[5], 0), "wait gate reset");
