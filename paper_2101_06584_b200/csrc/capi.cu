@@ -1366,7 +1366,8 @@ int mpfk_gemm_device_gathered(int width, uint64_t m, uint64_t n, uint64_t k, con
       g.M = (int)m, g.N = (int)n, g.K = (int)k;
       g.accumulate = 0;
       g.batch = 1, g.sa = g.sb = g.sc = 0;
-      kern::GateArgs gate_args{gate, gate + npan, (int)panel_rows, (int)band_rows};
+      // A is resident: every row counts as uploaded with the first panel
+      kern::GateArgs gate_args{gate, gate + npan, (int)panel_rows, (int)band_rows, (int)m, nullptr};
       dispatch_gemm_gated(width, g, gate_args, s);
       l = 1;
       ck(cudaStreamWaitEvent(s, D.evG[1], 0), "join gather");  // B complete when the stream is

@@ -262,8 +262,8 @@ struct GateArgs {
   // flags[p] covers B's panel p and A's panel p for rows < a_rows_first
   // only (the rows the first wave of tiles computes, uploaded first); the
   // remaining rows of A arrive after all panels and raise *a_rest
-  int a_rows_first;
-  const unsigned* a_rest;
+  int a_rows_first = 0x7fffffff;  // default: all of A is resident
+  const unsigned* a_rest = nullptr;
 };
 
 // out of line: the main loop keeps the plain kernel's code generation
