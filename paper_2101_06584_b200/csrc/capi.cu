@@ -341,6 +341,13 @@ double predicted_eff(const kern::GemmArgs& g, double steady) {
   return steady * useful * per_sm / std::ceil(per_sm);
 }
 
+// DD: the 32x32 tiles when the 64x64 grid would leave SMs unevenly loaded
+// (steady-state efficiencies from profiles/r01_tune.log); one rule for every
+// launch path (plain, split-K, fused all-gather, gated, host chunking)
+bool dd_small_tiles(const kern::GemmArgs& g) {
+  return predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944);
+}
+
 template <class Cfg>
 void launch_cfg(const kern::GemmArgs& g, cudaStream_t s) {
   configure_once<Cfg>();
@@ -428,7 +435,7 @@ void launch_pull_cfg(const kern::GemmArgs& g, const kern::PullB& P, cudaStream_t
 int dispatch_gemm_pull(int W, const kern::GemmArgs& g, const kern::PullB& P, cudaStream_t s) {
   switch (W) {
     case 2:
-      if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
+      if (dd_small_tiles(g))
         launch_pull_cfg<Cfg2s>(g, P, s);
       else
         launch_pull_cfg<Cfg2>(g, P, s);
@@ -460,7 +467,7 @@ void launch_splitk_cfg(const kern::GemmArgs& g, int klast, cudaStream_t s) {
 int dispatch_gemm_splitk(int W, const kern::GemmArgs& g, int klast, cudaStream_t s) {
   switch (W) {
     case 2:
-      if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
+      if (dd_small_tiles(g))
         launch_splitk_cfg<Cfg2s>(g, klast, s);
       else
         launch_splitk_cfg<Cfg2>(g, klast, s);
@@ -545,7 +552,7 @@ std::pair<int, int> launch_gated_cfg(const kern::GemmArgs& g, const kern::GateAr
 std::pair<int, int> dispatch_gemm_gated(int W, const kern::GemmArgs& g, const kern::GateArgs& G, cudaStream_t s) {
   switch (W) {
     case 2:
-      if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944)) return launch_gated_cfg<Cfg2s>(g, G, s);
+      if (dd_small_tiles(g)) return launch_gated_cfg<Cfg2s>(g, G, s);
       return launch_gated_cfg<Cfg2>(g, G, s);
     case 3: return launch_gated_cfg<Cfg3>(g, G, s);
     case 4: return launch_gated_cfg<Cfg4>(g, G, s);
@@ -556,7 +563,7 @@ std::pair<int, int> dispatch_gemm_gated(int W, const kern::GemmArgs& g, const ke
 int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s) {
   switch (W) {
     case 2:
-      if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
+      if (dd_small_tiles(g))
         launch_cfg<Cfg2s>(g, s);
       else
         launch_cfg<Cfg2>(g, s);

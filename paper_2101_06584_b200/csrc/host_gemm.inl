@@ -22,7 +22,7 @@ GatePlan gate_plan(int W, uint64_t m, uint64_t n) {
   GatePlan p{Cfg3::BM, Cfg3::BN, Cfg3::MINB, 0, 1.0};
   if (W == 4) p.bm = Cfg4::BM, p.bn = Cfg4::BN, p.minb = Cfg4::MINB;
   if (W == 2) {
-    if (predicted_eff<Cfg2s>(g, 0.90) > predicted_eff<Cfg2>(g, 0.944))
+    if (dd_small_tiles(g))
       p.bm = Cfg2s::BM, p.bn = Cfg2s::BN, p.minb = Cfg2s::MINB;
     else
       p.bm = Cfg2::BM, p.bn = Cfg2::BN, p.minb = Cfg2::MINB;
