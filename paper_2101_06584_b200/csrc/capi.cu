@@ -754,8 +754,10 @@ __global__ void binop_kernel(int op, long long count, const double* x, const dou
       arith::mp_mul<W>(a, b, c);
     else if (op == 2)
       arith::td_mul_q(a, b, c);
-    else
-      arith::td_add_merge(a, b, c);
+    else {
+      double zb[6];  // the ew kernel's ranked form (per-thread scratch here)
+      arith::td_add_merge_ranked(a, b, c, zb, 1);
+    }
 #pragma unroll
     for (int w = 0; w < W; ++w) r[i * W + w] = c[w];
   }

@@ -32,20 +32,24 @@ struct EwArgs {
 };
 
 template <int W, int OP>
-__device__ __forceinline__ void ew_one(const double* x, const double* y, double* r) {
+__device__ __forceinline__ void ew_one(const double* x, const double* y, double* r, double* zb) {
   if constexpr (OP == EW_SUB) {
     double ny[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) ny[w] = -y[w];  // exact sign flip (Ops::neg, eft.hpp:126)
     arith::mp_add<W>(x, ny, r);
   } else if constexpr (OP == EW_MUL) arith::mp_mul<W>(x, y, r);
-  else if constexpr (OP == EW_ADD_MERGE && W == 3) arith::td_add_merge(x, y, r);
+  else if constexpr (OP == EW_ADD_MERGE && W == 3) arith::td_add_merge_ranked(x, y, r, zb, 256);
   else arith::mp_add<W>(x, y, r);
 }
 
 // one thread = two adjacent columns (j, j+1), j even
 template <int W, int OP>
 __global__ void __launch_bounds__(256) ew_kernel(const EwArgs g) {
+  // merge-add: per-thread scatter slots for the ranked merge (slot k of
+  // thread t at zbuf[k * 256 + t]: conflict-free for any slot pattern)
+  __shared__ double zbuf[OP == EW_ADD_MERGE ? 6 * 256 : 1];
+  double* zb = zbuf + (OP == EW_ADD_MERGE ? threadIdx.x : 0);
   const int half = (g.cols + 1) / 2;
   const long long total = (long long)g.rows * half;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -59,9 +63,9 @@ __global__ void __launch_bounds__(256) ew_kernel(const EwArgs g) {
       const double2 bv = __ldcs(reinterpret_cast<const double2*>(g.b + w * g.pb + i * g.ldb + j));
       x0[w] = av.x, x1[w] = av.y, y0[w] = bv.x, y1[w] = bv.y;
     }
-    ew_one<W, OP>(x0, y0, r0);
+    ew_one<W, OP>(x0, y0, r0, zb);
     const bool second = j + 1 < g.cols;
-    if (second) ew_one<W, OP>(x1, y1, r1);
+    if (second) ew_one<W, OP>(x1, y1, r1, zb);
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       double* o = g.out + w * g.po + i * g.ldo + j;

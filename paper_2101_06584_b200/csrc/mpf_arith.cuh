@@ -464,6 +464,61 @@ MPFK_HD void td_add_merge(const double* x, const double* y, double* r) {
   vseb_3_6(e, r);
 }
 
+// td_add_merge with a ranked merge and a straight-line compress for the
+// common case, the exact state machines otherwise (bit-identical):
+//  * when both inputs are sorted by non-increasing magnitude (every
+//    normalised TD value is), the reference's greedy merge (eft.hpp:229-236;
+//    ties take x) is the stable merge: y[j] precedes x[i] iff |y[j]| >
+//    |x[i]|, so each element's output slot is its index plus a count of
+//    comparisons -- nine compares and a scatter through `zb` (slot k at
+//    zb[k * zstride]: per-thread shared memory on the device) instead of six
+//    rounds of data-dependent selects;
+//  * vseb(3 of 6) (eft.hpp:205-225) with the first three residuals nonzero
+//    emits the first three folds and returns: three quick-two-sums.
+// Unsorted inputs or a zero residual take merge6 / vseb_3_6 above.
+MPFK_HD void td_add_merge_ranked(const double* x, const double* y, double* r, double* zb, int zstride) {
+  const double ax0 = std::fabs(x[0]), ax1 = std::fabs(x[1]), ax2 = std::fabs(x[2]);
+  const double ay0 = std::fabs(y[0]), ay1 = std::fabs(y[1]), ay2 = std::fabs(y[2]);
+  double z[6];
+  if ((ax0 >= ax1) & (ax1 >= ax2) & (ay0 >= ay1) & (ay1 >= ay2)) {
+    const int px0 = 0 + (ay0 > ax0) + (ay1 > ax0) + (ay2 > ax0);
+    const int px1 = 1 + (ay0 > ax1) + (ay1 > ax1) + (ay2 > ax1);
+    const int px2 = 2 + (ay0 > ax2) + (ay1 > ax2) + (ay2 > ax2);
+    const int py0 = 0 + (ax0 >= ay0) + (ax1 >= ay0) + (ax2 >= ay0);
+    const int py1 = 1 + (ax0 >= ay1) + (ax1 >= ay1) + (ax2 >= ay1);
+    const int py2 = 2 + (ax0 >= ay2) + (ax1 >= ay2) + (ax2 >= ay2);
+    zb[px0 * zstride] = x[0];
+    zb[px1 * zstride] = x[1];
+    zb[px2 * zstride] = x[2];
+    zb[py0 * zstride] = y[0];
+    zb[py1 * zstride] = y[1];
+    zb[py2 * zstride] = y[2];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) z[k] = zb[k * zstride];
+  } else {
+    merge6(x, y, z);
+  }
+  double e[6];
+  double s = z[5];
+#pragma unroll
+  for (int i = 4; i >= 0; --i) {
+    double ss, ee;
+    two_sum(z[i], s, ss, ee);
+    e[i + 1] = ee;
+    s = ss;
+  }
+  e[0] = s;
+  double o0, r1, o1, r2, o2, r3;
+  qts(e[0], e[1], o0, r1);
+  qts(r1, e[2], o1, r2);
+  qts(r2, e[3], o2, r3);
+  if (nz(r1) & nz(r2) & nz(r3)) {
+    r[0] = o0, r[1] = o1, r[2] = o2;
+  } else {
+    vseb_3_6(e, r);
+  }
+}
+
 // td_mul_q, mpf.hpp:167-174: zero-extend, quad multiply, truncate (not a
 // library default; the comparison kernel of the paper's TD table).
 MPFK_HD void td_mul_q(const double* x, const double* y, double* r) {

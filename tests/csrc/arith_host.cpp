@@ -40,6 +40,11 @@ void hst_td_add_merge_batch(std::size_t count, const double* x, const double* y,
   for (std::size_t i = 0; i < count; ++i) td_add_merge(x + 3 * i, y + 3 * i, r + 3 * i);
 }
 
+void hst_td_add_merge_ranked_batch(std::size_t count, const double* x, const double* y, double* r) {
+  double zb[6];
+  for (std::size_t i = 0; i < count; ++i) td_add_merge_ranked(x + 3 * i, y + 3 * i, r + 3 * i, zb, 1);
+}
+
 void hst_renorm5_batch(std::size_t count, const double* c, double* r) {
   for (std::size_t i = 0; i < count; ++i) {
     const double* x = c + 5 * i;

@@ -165,6 +165,35 @@ def test_td_add_merge_host(H):
     want = np.empty_like(x)
     O.ref().ref_td_add_merge_batch(n, x.ctypes.data, y.ctypes.data, want.ctypes.data)
     assert not (r.view(np.uint64) != want.view(np.uint64)).any()
+    # the ranked merge + straight-line compress (the device ew kernel's form)
+    H.hst_td_add_merge_ranked_batch.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
+    r2 = np.empty_like(x)
+    H.hst_td_add_merge_ranked_batch(n, x.ctypes.data, y.ctypes.data, r2.ctypes.data)
+    assert not (r2.view(np.uint64) != want.view(np.uint64)).any()
+
+
+def test_td_add_merge_ranked_ties_and_orders(H):
+    """Ranked merge vs the reference on magnitude ties across the operands
+    (|x[i]| == |y[j]| with either sign, zeros of both signs), equal
+    components, unsorted operands and zero residuals."""
+    H.hst_td_add_merge_ranked_batch.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(77)
+    n = 60000
+    pool = np.array([0.0, -0.0, 1.0, -1.0, 0.5, -0.5, 2.0 ** -53, -2.0 ** -53, 2.0 ** -106, 3.0, 0.75, 2.0 ** -60])
+    x = rng.choice(pool, size=(n, 3))
+    y = rng.choice(pool, size=(n, 3))
+    # a third sorted by magnitude (the ranked path), a third with y = +-x, the rest as drawn
+    srt = lambda a: np.take_along_axis(a, np.argsort(-np.abs(a), axis=1, kind="stable"), axis=1)
+    x[: n // 3] = srt(x[: n // 3])
+    y[: n // 3] = srt(y[: n // 3])
+    y[n // 3: 2 * n // 3] = x[n // 3: 2 * n // 3] * rng.choice([1.0, -1.0], size=(n // 3, 1))
+    x = np.ascontiguousarray(x)
+    y = np.ascontiguousarray(y)
+    r = np.empty_like(x)
+    H.hst_td_add_merge_ranked_batch(n, x.ctypes.data, y.ctypes.data, r.ctypes.data)
+    want = np.empty_like(x)
+    O.ref().ref_td_add_merge_batch(n, x.ctypes.data, y.ctypes.data, want.ctypes.data)
+    assert not (r.view(np.uint64) != want.view(np.uint64)).any()
 
 
 def test_two_sum_sorted_equals_knuth(H):
