@@ -187,6 +187,31 @@ def test_baseline_config_sharded_sampled_rows(gpu_lib, W, n, wide):
     assert mismatches(C.data[:, rows, :], want) == 0
 
 
+@pytest.mark.parametrize("W,n,wide,nrows", [(2, 8192, False, 64), (3, 4096, True, 24), (4, 4096, True, 16)])
+def test_baseline_config_device_path_sampled_rows(gpu_lib, W, n, wide, nrows):
+    """The bench's device-resident path (mpfk_gemm_device, the kernel timed
+    for `value`) at the BASELINE full sizes: rows at tile edges (31/32, 63/64),
+    in the first and last tile bands and seeded random ones, bitwise against
+    the reference GEMM on those rows of A."""
+    import torch
+    P = gpu_lib
+    A = P.fill_baseline(W, n, n, 21, wide=wide).data
+    B = P.fill_baseline(W, n, n, 22, wide=wide).data
+    ld = A.shape[2]
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dC = torch.zeros_like(dA)
+    P.gemm_device(W, n, n, n, dA.data_ptr(), ld, n * ld, dB.data_ptr(), ld, n * ld, dC.data_ptr(), ld, n * ld)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(n + W)
+    fixed = [0, 31, 32, 63, 64, n // 2 - 1, n // 2, n - 65, n - 64, n - 33, n - 32, n - 1]
+    rows = sorted(set(fixed[:nrows // 2] + fixed[-(nrows // 4):] +
+                      rng.integers(0, n, nrows - nrows // 2 - nrows // 4).tolist()))
+    sub = np.ascontiguousarray(A[:, rows, :])
+    want = O.ref_gemm(sub, B, n, n)
+    got = dC[:, rows, :].cpu().numpy()
+    assert mismatches(got, want) == 0, rows
+
+
 @pytest.mark.parametrize("W", WIDTHS)
 def test_elementwise_kernels_bitwise(gpu_lib, W):
     """acceptance.cpp criterion 2 analog: device mpf::add/mul<W> lanewise
