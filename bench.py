@@ -41,6 +41,10 @@ WORKLOADS = {
 }
 DEFAULT_WORKLOAD = "dd8192"
 OPS_PER_MAC = {2: 20, 3: 132, 4: 218}
+# FP64 instructions the kernels execute per MAC (ncu sass op counts /
+# (m n k), profiles/r01b/metrics_*.csv): TD folds 11 operations on the
+# zero-extended fourth lane of td_add_q (DESIGN 4.1)
+EXEC_OPS_PER_MAC = {2: 20, 3: 121, 4: 218}
 NAMES = {2: "DD", 3: "TD", 4: "QD"}
 L2_BYTES = 126 * 2 ** 20
 METRIC = "MPF Gflops (2mnk/s), DD/TD/QD GEMM"
@@ -475,6 +479,8 @@ def run_mpfk(args, ws, rank, local):
                          "frac": round(achieved / (peak_ops / 1e9), 4),
                          "frac_of_nominal": round(achieved / (NOMINAL_FP64_LANE_OPS / 1e9), 4),
                          "ops_per_mac": ops, "kernel_ms": round(t_kern, 3),
+                         "ops_per_mac_executed": EXEC_OPS_PER_MAC[W],
+                         "frac_executed": round(achieved * EXEC_OPS_PER_MAC[W] / ops / (peak_ops / 1e9), 4),
                          "peak_source": "measured on this GPU by mpfk_fp64_peak (DFMA chains); "
                                         "MEASURED_PEAKS.json has no FP64 entry",
                          "traffic": traffic,
