@@ -113,6 +113,7 @@ struct TileCfg {
   // same order): bit-identical, and the common path has no branch
   static constexpr int FASTR = (W_ >= 3) ? FASTR_ : 0;
   static constexpr int SNAP = FASTR ? THREADS * TM * TN * W : 0;  // doubles
+  static_assert(!FASTR || THREADS % 32 == 0, "the warp-level redo votes over full warps");
   static constexpr int APAD = 2, BPAD = 2;  // keep 16 B row alignment, spread banks
   static constexpr int AS = BK + APAD;      // A tile row stride (doubles), [BM][AS]
   static constexpr int BS = BN + BPAD;      // B tile row stride, [BK][BS]
