@@ -2,7 +2,7 @@
 FASTR redo path) and the host-buffer gated (page-locked) and chunked
 (pageable) paths, bitwise against the reference; prints the redo count.
 (compute-sanitizer is closed on the GPU pool, so this is the small-case
-check instead.)  python scripts/sanitize.py"""
+check instead.)  python scripts/smallcheck.py"""
 import os
 import sys
 
