@@ -6,7 +6,6 @@ how many CTAs in the first wave and the start-time spread.
 import collections
 import ctypes as C
 import os
-import sys
 
 import numpy as np
 import torch
