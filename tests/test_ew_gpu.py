@@ -62,3 +62,30 @@ def test_ew_large_vectors(gpu_lib, W):
         P.ew_apply_into(out, a, b, P.EwOp[op], P.KernelVariant.SIMD_LOADSTORE)
         want = O.ref_ew(W, op, a.data, b.data, n)
         assert mismatches(out.data, want) == 0
+
+
+def test_ew_add_merge_ranked_and_fallback_paths(gpu_lib):
+    """The device merge-add (mpf_arith.cuh:td_add_merge_ranked) on operands
+    that take every branch: magnitude-sorted (ranked merge through the
+    per-thread shared-memory slots), ties across the operands with either
+    sign, unsorted components (the greedy merge6 fallback), and exactly
+    cancelling pairs (zero residuals: the vseb_3_6 fallback) -- bit for bit
+    against the reference's td_add_merge (mpf.hpp:125-131)."""
+    P = gpu_lib
+    rng = np.random.default_rng(125)
+    rows, cols = 64, 257
+    pool = np.array([0.0, -0.0, 1.0, -1.0, 0.5, -0.5, 0.75, 3.0, 2.0 ** -53, -2.0 ** -53, 2.0 ** -106, 2.0 ** -60])
+    a = O.planes(3, rows, cols)
+    b = O.planes(3, rows, cols)
+    a[:, :, :cols] = rng.choice(pool, size=(3, rows, cols))
+    b[:, :, :cols] = rng.choice(pool, size=(3, rows, cols))
+    srt = np.argsort(-np.abs(a[:, :16, :cols]), axis=0, kind="stable")
+    a[:, :16, :cols] = np.take_along_axis(a[:, :16, :cols], srt, axis=0)
+    srt = np.argsort(-np.abs(b[:, :16, :cols]), axis=0, kind="stable")
+    b[:, :16, :cols] = np.take_along_axis(b[:, :16, :cols], srt, axis=0)
+    b[:, 16:32, :cols] = -a[:, 16:32, :cols]          # exact cancellation
+    b[:, 32:40, :cols] = a[:, 32:40, :cols]           # ties with the same sign
+    want = O.ref_ew(3, "add_merge", a, b, cols)
+    out = P.MPMatrix(3, rows, cols)
+    P.ew_apply_into(out, to_mp(a, cols), to_mp(b, cols), P.EwOp.add_merge, P.KernelVariant.SIMD_LOADSTORE)
+    assert mismatches(out.data, want) == 0
