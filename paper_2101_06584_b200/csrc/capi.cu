@@ -299,11 +299,14 @@ void grow(double*& p, size_t& cap, size_t bytes) {
 // most -- it caps registers so 2-3 CTAs share each SM's FP64 pipe.
 using Cfg2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 2, 16, 2>;     // DD, large problems
 using Cfg2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 2, 16, 4>;    // DD, few waves
-// TD / QD: branch-free renorm5 in the k loop with an exact warp-level redo
-// of any k-tile that met a zero-residual input (TileCfg::FASTR,
-// profiles/r01_tune_fastr.log: QD n=4096 0.9225 -> 0.930, TD n=1024 +2.5 %).
-using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1>;  // TD
-using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1>;  // QD
+// TD / QD: branch- and select-free common paths in the k loop with an exact
+// warp-level redo of any k-tile that met an input outside them
+// (TileCfg::FASTR / VSEBF; profiles/r01_tune_fastr.log, r01_tune_levels.log):
+// TD renorm5 paths A/B + td_mul's vseb common case (n=4096 0.978 -> 1.030 of
+// peak in counted ops), QD renorm5 path A only (0.928 -> 0.962).  Path B is
+// common for TD (its zero-extended fourth lane), so TD keeps it in the fast form.
+using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1>;  // TD: renorm5 A/B, vseb fast
+using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 2>;  // QD: renorm5 path A
 
 template <class Cfg>
 void configure_once() {

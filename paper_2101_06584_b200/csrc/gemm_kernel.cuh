@@ -94,7 +94,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // and share their A and B panels in L2 instead of streaming all of B per
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
-          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0>
+          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0, int VSEBF_ = 0>
 struct TileCfg {
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
   static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
@@ -111,7 +111,8 @@ struct TileCfg {
   // restores its chains from a shared-memory snapshot taken at the k-tile
   // start and recomputes the k-tile with the exact form (same smem stage,
   // same order): bit-identical, and the common path has no branch
-  static constexpr int FASTR = (W_ >= 3) ? FASTR_ : 0;
+  static constexpr int FASTR = (W_ >= 3) ? FASTR_ : 0;  // renorm5_t level (1: paths A/B, 2: path A)
+  static constexpr bool VSEBF = FASTR && VSEBF_;          // td_mul's vseb common case in the fast pass
   static constexpr int SNAP = FASTR ? THREADS * TM * TN * W : 0;  // doubles
   static_assert(!FASTR || THREADS % 32 == 0, "the warp-level redo votes over full warps");
   static constexpr int APAD = 2, BPAD = 2;  // keep 16 B row alignment, spread banks
@@ -325,8 +326,8 @@ __device__ __forceinline__ void mac_step_fast(double (&acc)[Cfg::TM][Cfg::TN][Cf
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       double p[W];
-      arith::mp_mul_f<W, true>(a[i], b[j], p, rare);
-      arith::mp_add_f<W, true>(acc[i][j], p, acc[i][j], rare);
+      arith::mp_mul_f<W, Cfg::FASTR, Cfg::VSEBF>(a[i], b[j], p, rare);
+      arith::mp_add_f<W, Cfg::FASTR>(acc[i][j], p, acc[i][j], rare);
     }
 }
 

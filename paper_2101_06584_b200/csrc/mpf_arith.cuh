@@ -162,13 +162,17 @@ MPFK_HD void three_sum2(double a, double b, double c, double& s, double& e) {
 // value, including the +0 initialisers of s2/s3 (eft.hpp:251).
 // ---------------------------------------------------------------------------
 //
-// kFast: paths A/B only, branch-free, and `rare` is set when the input needs
-// paths C/D (a zero residual in the first two forward steps) -- the result
-// is then NOT the reference's, and the caller must recompute with the exact
-// form (gemm_kernel.cuh: a warp redoes its k-tile from a snapshot of C).
+// kFast (the GEMM inner loop; the result is then NOT the reference's when
+// `rare` gets set, and the caller recomputes with the exact form --
+// gemm_kernel.cuh: a warp redoes its k-tile from a snapshot of C):
+//   1: paths A/B, branch-free (two selects); `rare` for paths C/D, a zero
+//      residual in the first two forward steps;
+//   2: path A only, branch- and select-free; `rare` also for path B (a zero
+//      third residual) -- a win when path B is rare (QD), a loss when it is
+//      common (TD's zero-extended fourth lane makes it so).
 // Without the branch the compiler interleaves a thread's independent chains
 // across the renormalisation (TD/QD GEMM +2-3 %).
-template <bool kFast>
+template <int kFast>
 MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, double& r0,
                        double& r1, double& r2, double& r3, bool& rare) {
   double t;
@@ -181,8 +185,20 @@ MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, do
   qts(c0, c1, s0, s1);
   qts(s1, c2, u, s2);
   const bool ab = nz(s1) & nz(s2);
-  if (kFast) rare |= !ab;
-  if (kFast || ab) {
+  if (kFast == 1) rare |= !ab;
+  if (kFast == 2) {
+    // path A only (all three forward residuals nonzero, eft.hpp:255-257):
+    // no selects; path B (s3 == 0) and C/D count as rare
+    double v, s3;
+    qts(s2, c3, v, s3);
+    rare |= !(ab & nz(s3));
+    r0 = s0;
+    r1 = u;
+    r2 = v;
+    r3 = add(s3, c4);
+    return;
+  }
+  if (kFast == 1 || ab) {
     // path A (s3 != 0: s3 += c4) or path B (s3 == 0: s2 += c4), eft.hpp:255-260
     double v, s3;
     qts(s2, c3, v, s3);
@@ -230,7 +246,7 @@ MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, do
 MPFK_HD void renorm5(double c0, double c1, double c2, double c3, double c4, double& r0,
                      double& r1, double& r2, double& r3) {
   bool rare = false;
-  renorm5_t<false>(c0, c1, c2, c3, c4, r0, r1, r2, r3, rare);
+  renorm5_t<0>(c0, c1, c2, c3, c4, r0, r1, r2, r3, rare);
 }
 
 // vseb with k = 2 output slots over n = 3 inputs (the only use on the path:
@@ -273,7 +289,7 @@ MPFK_HD void dd_mul(const double* x, const double* y, double* r) {
 // qd_add, mpf.hpp:178-196 (63 ops + renorm5).  With Trunc3 the fourth
 // output is not produced (td_add_q drops it, mpf.hpp:141), which lets the
 // compiler delete the dead tail of renorm5.
-template <bool Trunc3 = false, bool kFast = false>
+template <bool Trunc3 = false, int kFast = 0>
 MPFK_HD void qd_add(const double* x, const double* y, double* r, bool& rare) {
   double s0, t0, s1, t1, s2, t2, s3, t3;
   two_sum(x[0], y[0], s0, t0);
@@ -291,12 +307,12 @@ MPFK_HD void qd_add(const double* x, const double* y, double* r, bool& rare) {
 template <bool Trunc3 = false>
 MPFK_HD void qd_add(const double* x, const double* y, double* r) {
   bool rare = false;
-  qd_add<Trunc3, false>(x, y, r, rare);
+  qd_add<Trunc3, 0>(x, y, r, rare);
 }
 
 // qd_mul, mpf.hpp:198-238 (111 ops + renorm5), including the pre-combined
 // operand pairs that keep it bitwise commutative (mpf.hpp:214-221).
-template <bool kFast>
+template <int kFast>
 MPFK_HD void qd_mul_t(const double* x, const double* y, double* r, bool& rare) {
   double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
   two_prod(x[0], y[0], p0, q0);
@@ -329,7 +345,7 @@ MPFK_HD void qd_mul_t(const double* x, const double* y, double* r, bool& rare) {
 }
 MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
   bool rare = false;
-  qd_mul_t<false>(x, y, r, rare);
+  qd_mul_t<0>(x, y, r, rare);
 }
 
 // td_add_q, mpf.hpp:135-142: zero-extend with +0, quad add, truncate.
@@ -347,7 +363,7 @@ MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
 //  * t0 + t3 with t3 = +0 stays (same reason).
 // 11 of td_add_q's 85 FP64 operations disappear; results are unchanged
 // (tests/test_arith_host.py sweeps signed zeros against the reference).
-template <bool kFast>
+template <int kFast>
 MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, bool& rare) {
   double s0, t0, s1, t1, s2, t2;
   two_sum(x[0], y[0], s0, t0);
@@ -366,7 +382,7 @@ MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, bool& rare)
 }
 MPFK_HD void td_add_q(const double* x, const double* y, double* r) {
   bool rare = false;
-  td_add_q_t<false>(x, y, r, rare);
+  td_add_q_t<0>(x, y, r, rare);
 }
 
 // td_add_q without the folds (the literal zero-extend + qd_add); kept for
@@ -377,8 +393,10 @@ MPFK_HD void td_add_q_unfolded(const double* x, const double* y, double* r) {
   qd_add<true>(xx, yy, r);
 }
 
-// td_mul, mpf.hpp:146-163 (41 ops + vseb).
-MPFK_HD void td_mul(const double* x, const double* y, double* r) {
+// td_mul, mpf.hpp:146-163 (41 ops + vseb).  kFast: vseb's common case only
+// (first residual nonzero: the two folds are the outputs), `rare` otherwise.
+template <bool kFast>
+MPFK_HD void td_mul_t(const double* x, const double* y, double* r, bool& rare) {
   double z00s, z00e, z01s, z01e, z10s, z10e;
   two_prod(x[0], y[0], z00s, z00e);
   two_prod(x[0], y[1], z01s, z01e);
@@ -398,7 +416,19 @@ MPFK_HD void td_mul(const double* x, const double* y, double* r) {
   two_sum(b0, s, s, e2);
   two_sum(z00s, s, e0, e1);
   r[0] = e0;
-  vseb_2_3(e1, e2, e3, r[1], r[2]);
+  if (kFast) {
+    double a, rr, b, r2;
+    qts(e1, e2, a, rr);
+    rare |= !nz(rr);
+    qts(rr, e3, b, r2);
+    r[1] = a, r[2] = b;
+  } else {
+    vseb_2_3(e1, e2, e3, r[1], r[2]);
+  }
+}
+MPFK_HD void td_mul(const double* x, const double* y, double* r) {
+  bool rare = false;
+  td_mul_t<false>(x, y, r, rare);
 }
 
 // merge_by_magnitude, eft.hpp:229-236: stable merge of two 3-term lists by
@@ -530,23 +560,6 @@ MPFK_HD void td_mul_q(const double* x, const double* y, double* r) {
 }
 
 // Library width defaults, mpf.hpp:242-260.
-// kFast (GEMM inner loop): renorm5 paths A/B only; `rare` reports an input
-// that needed paths C/D (the result must then be recomputed exactly).  DD
-// has no data-dependent branch, so its kFast form is the exact one.
-template <int W, bool kFast>
-MPFK_HD void mp_add_f(const double* x, const double* y, double* r, bool& rare) {
-  if constexpr (W == 2) dd_add(x, y, r);
-  else if constexpr (W == 3) td_add_q_t<kFast>(x, y, r, rare);
-  else qd_add<false, kFast>(x, y, r, rare);
-}
-
-template <int W, bool kFast>
-MPFK_HD void mp_mul_f(const double* x, const double* y, double* r, bool& rare) {
-  if constexpr (W == 2) dd_mul(x, y, r);
-  else if constexpr (W == 3) td_mul(x, y, r);
-  else qd_mul_t<kFast>(x, y, r, rare);
-}
-
 template <int W>
 MPFK_HD void mp_add(const double* x, const double* y, double* r) {
   if constexpr (W == 2) dd_add(x, y, r);
@@ -559,6 +572,24 @@ MPFK_HD void mp_mul(const double* x, const double* y, double* r) {
   if constexpr (W == 2) dd_mul(x, y, r);
   else if constexpr (W == 3) td_mul(x, y, r);
   else qd_mul(x, y, r);
+}
+
+// GEMM inner-loop forms: kRenorm = renorm5_t level (0 exact, 1 paths A/B,
+// 2 path A), kVseb = td_mul's vseb common case only; `rare` reports an input
+// that left the fast form (the result must then be recomputed exactly).  DD
+// has no data-dependent branch, so its fast form is the exact one.
+template <int W, int kRenorm>
+MPFK_HD void mp_add_f(const double* x, const double* y, double* r, bool& rare) {
+  if constexpr (W == 2) dd_add(x, y, r);
+  else if constexpr (W == 3) td_add_q_t<kRenorm>(x, y, r, rare);
+  else qd_add<false, kRenorm>(x, y, r, rare);
+}
+
+template <int W, int kRenorm, bool kVseb>
+MPFK_HD void mp_mul_f(const double* x, const double* y, double* r, bool& rare) {
+  if constexpr (W == 2) dd_mul(x, y, r);
+  else if constexpr (W == 3) td_mul_t<kVseb>(x, y, r, rare);
+  else qd_mul_t<kRenorm>(x, y, r, rare);
 }
 
 // Algorithmic FP64 operations per multiply-add (reference sequence, renorm5

@@ -90,6 +90,11 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 0, 1>>,                                 \
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 0, 1>>}
 
+#define EF2(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, LV, VF)                                          \
+  {W, "fastr" #LV "v" #VF "/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB, \
+   run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 0, LV, VF>>,                            \
+   info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, 0, 0, LV, VF>>}
+
 #define F(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX)                                                \
   {W, #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/g" #GM "/mb" #MB "/fixk" #FX,  \
    run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX>>,                                      \
@@ -98,6 +103,11 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
 const Entry kEntries[] = {
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
     E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // DD few-wave product
+    EF2(3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 1, 0),  // TD: renorm A/B, vseb exact
+    EF2(3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 1, 1),  // TD: renorm A/B, vseb fast
+    EF2(3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 2, 0),  // TD: renorm A only
+    EF2(4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 1, 0),  // QD: renorm A/B
+    EF2(4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 2, 0),  // QD: renorm A only
     EF(3, 32, 32, 8, 2, 2, 2, 1, 16, 3),   // branch-free renorm5 + warp redo
     EF(3, 32, 32, 16, 2, 2, 2, 1, 16, 2),
     EF(3, 16, 32, 16, 1, 2, 2, 1, 16, 3),
