@@ -43,8 +43,9 @@ DEFAULT_WORKLOAD = "dd8192"
 OPS_PER_MAC = {2: 20, 3: 132, 4: 218}
 # FP64 instructions the kernels execute per MAC (ncu sass op counts /
 # (m n k), profiles/r01b/metrics_*.csv): TD folds 11 operations on the
-# zero-extended fourth lane of td_add_q (DESIGN 4.1)
-EXEC_OPS_PER_MAC = {2: 20, 3: 121, 4: 218}
+# zero-extended fourth lane of td_add_q (DESIGN 4.1) and, in the fast pass,
+# skips the two operations of vseb's residual that only its rare path reads
+EXEC_OPS_PER_MAC = {2: 20, 3: 119, 4: 218}
 NAMES = {2: "DD", 3: "TD", 4: "QD"}
 L2_BYTES = 126 * 2 ** 20
 METRIC = "MPF Gflops (2mnk/s), DD/TD/QD GEMM"
