@@ -172,7 +172,7 @@ MPFK_HD void three_sum2(double a, double b, double c, double& s, double& e) {
 //      common (TD's zero-extended fourth lane makes it so).
 // Without the branch the compiler interleaves a thread's independent chains
 // across the renormalisation (TD/QD GEMM +2-3 %).
-template <int kFast>
+template <int kFast, bool kTrunc3 = false>
 MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, double& r0,
                        double& r1, double& r2, double& r3, bool& rare) {
   double t;
@@ -196,6 +196,17 @@ MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, do
     r1 = u;
     r2 = v;
     r3 = add(s3, c4);
+    return;
+  }
+  if (kFast == 1 && kTrunc3) {
+    // paths A/B when the fourth output is dropped (td_add_q): path A keeps
+    // r2 = v, path B folds c4 into it -- the same add either way, one select
+    double v, s3;
+    qts(s2, c3, v, s3);
+    r0 = s0;
+    r1 = u;
+    r2 = sel(nz(s3), v, add(v, c4));
+    r3 = 0.0;  // not an output (the caller truncates)
     return;
   }
   if (kFast == 1 || ab) {
@@ -378,7 +389,7 @@ MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, bool& rare)
   t0 = add(0.0, ue);
   t0 = add(add(t0, t1), 0.0);
   double r3;
-  renorm5_t<kFast>(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3, rare);
+  renorm5_t<kFast, true>(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3, rare);
 }
 MPFK_HD void td_add_q(const double* x, const double* y, double* r) {
   bool rare = false;
