@@ -344,6 +344,7 @@ def run_mpfk(args, ws, rank, local):
     if use_dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    P.gemm_redo_count(reset=True)  # TD/QD fast-pass redo counter (synchronises; outside the timed region)
     clocks.start()
     time.sleep(0.3)
     launches[0] = 0
@@ -361,6 +362,7 @@ def run_mpfk(args, ws, rank, local):
     if use_dist:
         dist.barrier()
     clk = clocks.stop()
+    redo = P.gemm_redo_count(reset=True)
     check = None
     if args.check and rows:
         ref = torch.zeros_like(dC)
@@ -481,6 +483,9 @@ def run_mpfk(args, ws, rank, local):
                          "frac_of_nominal": round(achieved / (NOMINAL_FP64_LANE_OPS / 1e9), 4),
                          "ops_per_mac": ops, "kernel_ms": round(t_kern, 3),
                          "ops_per_mac_executed": EXEC_OPS_PER_MAC[W],
+                         # TD/QD: warp k-tiles per step that left the branch-free fast
+                         # pass and were recomputed exactly (DESIGN 4.2)
+                         "redo_warp_ktiles_per_step": round(redo / max(args.steps, 1), 1),
                          "frac_executed": round(achieved * EXEC_OPS_PER_MAC[W] / ops / (peak_ops / 1e9), 4),
                          "peak_source": "measured on this GPU by mpfk_fp64_peak (DFMA chains); "
                                         "MEASURED_PEAKS.json has no FP64 entry",
