@@ -297,8 +297,10 @@ void grow(double*& p, size_t& cap, size_t bytes) {
 // Tile configurations chosen by the sweep in scripts/tune.py over
 // csrc/tune.cu (profiles/r01_tune.log): the occupancy floor (MINB) matters
 // most -- it caps registers so 2-3 CTAs share each SM's FP64 pipe.
-using Cfg2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 2, 16, 2>;     // DD, large problems
-using Cfg2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 2, 16, 4>;    // DD, few waves
+// DD: full k-tiles as one straight-line 16-step block (FIXK, KUNROLL 16) and
+// one barrier per k-tile (ONEBAR): +1 % (profiles/r01_tune_dd_fixk.log)
+using Cfg2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1>;   // DD, large problems
+using Cfg2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1>;  // DD, few waves
 // TD / QD: branch- and select-free common paths in the k loop with an exact
 // warp-level redo of any k-tile that met an input outside them
 // (TileCfg::FASTR / VSEBF; profiles/r01_tune_fastr.log, r01_tune_levels.log):

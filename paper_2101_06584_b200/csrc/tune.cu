@@ -103,6 +103,11 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
 const Entry kEntries[] = {
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
     E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // DD few-wave product
+    F(2, 64, 64, 16, 4, 4, 2, 8, 16, 2, 1),   // DD product with a constant-trip k loop
+    F(2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1),
+    {2, "2/64x64x16/4x4/st2/ku16/g16/mb2/fixk1/onebar",
+     run_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1>>, info_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1>>},
+    F(2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1),  // DD few-wave tiles, same
     EF2(3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 1, 0),  // TD: renorm A/B, vseb exact
     EF2(3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 1, 1),  // TD: renorm A/B, vseb fast
     EF2(3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 2, 0),  // TD: renorm A only
