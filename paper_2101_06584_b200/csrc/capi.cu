@@ -308,7 +308,10 @@ using Cfg2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1>;  // DD, fe
 // peak in counted ops), QD renorm5 path A only (0.928 -> 0.962).  Path B is
 // common for TD (its zero-extended fourth lane), so TD keeps it in the fast form.
 using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1>;  // TD: renorm5 A/B, vseb fast
-using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 2>;  // QD: renorm5 path A
+using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>;  // QD: renorm5 path A, 4-step unroll
+// the copy-engine-gated QD launch keeps the 1-step loop: with the 4-step
+// straight-line k-tiles it ran 25 ms slower at n=4096 (e2e 891 vs 864 ms)
+using Cfg4g = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 2>;
 
 template <class Cfg>
 void configure_once() {
@@ -560,7 +563,7 @@ std::pair<int, int> dispatch_gemm_gated(int W, const kern::GemmArgs& g, const ke
       if (dd_small_tiles(g)) return launch_gated_cfg<Cfg2s>(g, G, s);
       return launch_gated_cfg<Cfg2>(g, G, s);
     case 3: return launch_gated_cfg<Cfg3>(g, G, s);
-    case 4: return launch_gated_cfg<Cfg4>(g, G, s);
+    case 4: return launch_gated_cfg<Cfg4g>(g, G, s);
     default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
   }
 }

@@ -442,8 +442,13 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
 #pragma unroll
           for (int w = 0; w < W; ++w) snap[((i * TN + j) * W + w) * Cfg::THREADS] = acc[i][j][w];
       bool rare = false;
+      if (Cfg::FIXK && kk == 0 && kend == BK) {
 #pragma unroll Cfg::KUNROLL
-      for (int q = kk; q < kend; ++q) mac_step_fast<Cfg>(acc, As, Bs, tx, ty, q, rare);
+        for (int q = 0; q < BK; ++q) mac_step_fast<Cfg>(acc, As, Bs, tx, ty, q, rare);
+      } else {
+#pragma unroll Cfg::KUNROLL
+        for (int q = kk; q < kend; ++q) mac_step_fast<Cfg>(acc, As, Bs, tx, ty, q, rare);
+      }
       if (__any_sync(0xffffffffu, rare)) {  // rare: this warp redoes the k-tile exactly
         if ((threadIdx.x & 31) == 0) atomicAdd(&g_fastr_redo, 1ull);
 #pragma unroll

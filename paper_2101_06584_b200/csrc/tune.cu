@@ -103,6 +103,18 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
 const Entry kEntries[] = {
     E(2, 64, 64, 16, 4, 4, 2, 2, 16, 2),  // DD product
     E(2, 32, 32, 16, 2, 2, 2, 2, 16, 4),  // DD few-wave product
+    {3, "fixk/3/ku2", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 2, 16, 2, 1, 0, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 2, 16, 2, 1, 0, 1, 1>>},
+    {3, "fixk/3/ku4/onebar", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 1, 1>>},
+    {3, "fixk/3/ku16/onebar", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 16, 16, 2, 1, 1, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 16, 16, 2, 1, 1, 1, 1>>},
+    {4, "fixk/4/ku2", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 2, 16, 2, 1, 0, 2>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 2, 16, 2, 1, 0, 2>>},
+    {4, "fixk/4/ku4/onebar", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>>},
+    {4, "fixk/4/ku1/onebar", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 1, 1, 2>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 1, 1, 2>>},
     F(2, 64, 64, 16, 4, 4, 2, 8, 16, 2, 1),   // DD product with a constant-trip k loop
     F(2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1),
     {2, "2/64x64x16/4x4/st2/ku16/g16/mb2/fixk1/onebar",
