@@ -286,11 +286,13 @@ int mpfk_eft_batch(int op, uint64_t count, const double *a, const double *b, dou
 void mpfk_op_counters_reset(void);
 void mpfk_op_counters_read(uint64_t *adds, uint64_t *muls, uint64_t *leaf_multiplies);
 
-/* TD/QD GEMM kernels run each k-tile with the branch-free renormalisation
- * (renorm5 paths A/B, eft.hpp:255-260) and recompute, exactly, any warp's
- * k-tile that met an input needing paths C/D (eft.hpp:261-286).  Number of
- * such recomputed warp k-tiles on the current device since the last reset
- * (synchronises the device).  No reference counterpart; for tests. */
+/* TD/QD GEMM kernels run each k-tile with branch-free common paths (QD:
+ * renorm5 path A, eft.hpp:255-257; TD: renorm5 paths A/B, eft.hpp:255-260,
+ * and td_mul's vseb with a nonzero first residual, eft.hpp:205-225) and
+ * recompute, exactly, any warp's k-tile that met an input outside them.
+ * Number of such recomputed warp k-tiles on the current device since the
+ * last reset (synchronises the device).  No reference counterpart; for
+ * tests and the bench line. */
 int mpfk_gemm_redo_count(uint64_t *count, int reset);
 
 /* ---- pinned host memory for MPMatrix-style buffers ----------------------- */
