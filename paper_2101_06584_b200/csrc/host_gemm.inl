@@ -69,8 +69,12 @@ void host_gemm_gated(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, D
   grow(D.dA, D.capA, sizeof(double) * W * std::max<uint64_t>(m * lda, 1));
   grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
   grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(m * ldc, 1));
-  // K panels: >= 256 k steps, at most 32, a multiple of BK = 16 rows each
-  const uint64_t np0 = std::max<uint64_t>(1, std::min<uint64_t>(32, K / 256));
+  // K panels: >= 128 k steps, at most 32, a multiple of BK = 16 rows each.
+  // The kernel starts once the first panel has landed, so smaller panels
+  // start it sooner, but A's panel is a column slab whose 2D copy slows down
+  // with narrow rows (measured: 64-k panels cost DD n=1024 e2e 4 %, helped
+  // TD/QD n=1024 2 %; 256-k panels idle the GPU for the first 1/4 of A+B)
+  const uint64_t np0 = std::max<uint64_t>(1, std::min<uint64_t>(32, K / 128));
   const uint64_t pk = ((K + np0 - 1) / np0 + 15) / 16 * 16;
   const uint64_t npan = (K + pk - 1) / pk;
   const uint64_t band_rows = 256;  // a multiple of every configuration's BM
