@@ -310,7 +310,9 @@ using Cfg2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1>;  // DD, fe
 using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1>;  // TD: renorm5 A/B, vseb fast
 using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>;  // QD: renorm5 path A, 4-step unroll
 // the copy-engine-gated QD launch keeps the 1-step loop: with the 4-step
-// straight-line k-tiles it ran 25 ms slower at n=4096 (e2e 891 vs 864 ms)
+// straight-line k-tiles and one barrier per k-tile it ran 25 ms slower at
+// n=4096 (e2e 891 vs 864 ms; the per-panel flag wait after the k-tile's
+// barrier is the culprit -- 4-step tiles with two barriers measure 867 ms)
 using Cfg4g = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 2>;
 
 template <class Cfg>
