@@ -218,6 +218,24 @@ int mpfk_gemm_device_gathered(int width, uint64_t m, uint64_t n, uint64_t k, con
                               uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, int nsrc,
                               const double *const *src, const uint64_t *src_row0,
                               uint64_t panel_rows, void *stream, int *launches);
+/* All-gather -> GEMM with no in-kernel waiting (the default multi-GPU
+ * transport of bench.py): the copy engines gather B from the source slices
+ * (same table as mpfk_gemm_device_gathered, up to 64 slices) on an internal
+ * stream in ascending K panels -- a short first panel of head_rows rows
+ * (0: 64), each next one 4x longer, at most 8 -- and one GEMM launch per
+ * panel on `stream` waits on that panel's event only (panels after the
+ * first continue the chains kept in C, as mpfk_gemm_device_acc).  Every
+ * panel's compute covers the gather of the next, so only the first panel's
+ * transfer is exposed, the gather costs no SM time, and no kernel spins on
+ * a flag.  Bit-identical to mpfk_gemm_device; after the call (in stream
+ * order) B holds the whole matrix.
+ * Replaces, across GPUs, the reference's worker fan-out over row blocks
+ * (linalg.hpp:402-433), which shares B through host memory. */
+int mpfk_gemm_device_staged(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                            uint64_t lda, uint64_t a_plane, double *B, uint64_t ldb,
+                            uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, int nsrc,
+                            const double *const *src, const uint64_t *src_row0,
+                            uint64_t head_rows, void *stream, int *launches);
 /* device memory and CUDA IPC plumbing for the fused path (one process per
  * GPU): handles are 64-byte cudaIpcMemHandle_t blobs. */
 int mpfk_device_alloc(uint64_t bytes, void **ptr);

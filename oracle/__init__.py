@@ -88,6 +88,13 @@ def ref():
         L.ref_td_add_merge_batch.argtypes = [_S, _D, _D, _D]
         L.ref_td_mul_q_batch.argtypes = [_S, _D, _D, _D]
         L.ref_eft_batch.argtypes = [C.c_int, _S, _D, _D, _D, _D]
+        L.ref_prep_new.argtypes = [C.c_int, _S, _S, _S, _D, _S, _D, _S]
+        L.ref_prep_new.restype = C.c_void_p
+        L.ref_prep_run.argtypes = [C.c_void_p, _S, C.c_int, C.c_uint, C.POINTER(C.c_double)]
+        L.ref_prep_result.argtypes = [C.c_void_p, _D, _S]
+        L.ref_prep_free.argtypes = [C.c_void_p]
+        L.ref_prep_with_a.argtypes = [C.c_void_p, _S, _D, _S]
+        L.ref_prep_with_a.restype = C.c_void_p
         _ref = L
     return _ref
 
@@ -205,3 +212,77 @@ def ref_strassen(A, B, K, n, cutoff=64, n_min=32, variant=0, workers=1):
     if rc:
         raise ValueError(ref().ref_last_error().decode())
     return Cm
+
+
+class RefPrepared:
+    """The reference's matmul_block_parallel_into on operands converted to
+    mpfkit MPMatrix objects ONCE; run() returns the seconds of one call,
+    timed inside C++ (ref_prep_run).  The CPU baseline of bench.py."""
+
+    def __init__(self, A: np.ndarray, B: np.ndarray, K: int, n: int):
+        W, m, lda = A.shape
+        self.W, self.m, self.n = W, m, n
+        self.h = None
+        A = np.ascontiguousarray(A)
+        B = np.ascontiguousarray(B)
+        self.h = ref().ref_prep_new(W, m, K, n, _p(A), lda, _p(B), B.shape[2])
+        if not self.h:
+            raise ValueError(ref().ref_last_error().decode())
+
+    def with_a(self, A: np.ndarray) -> "RefPrepared":
+        """A second problem over the same reference B (shared, not copied)."""
+        W, m, lda = A.shape
+        A = np.ascontiguousarray(A)
+        o = RefPrepared.__new__(RefPrepared)
+        o.W, o.m, o.n = W, m, self.n
+        o.h = ref().ref_prep_with_a(self.h, m, _p(A), lda)
+        if not o.h:
+            raise ValueError(ref().ref_last_error().decode())
+        return o
+
+    def run(self, workers, n_min=32, variant=2) -> float:
+        s = C.c_double(0.0)
+        if ref().ref_prep_run(self.h, n_min, variant, workers, C.byref(s)):
+            raise ValueError(ref().ref_last_error().decode())
+        return s.value
+
+    def result(self) -> np.ndarray:
+        out = np.zeros((self.W, self.m, (self.n + 3) & ~3), dtype=np.float64)
+        ref().ref_prep_result(self.h, _p(out), out.shape[2])
+        return out
+
+    def close(self):
+        if self.h:
+            ref().ref_prep_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def host_cpu_info() -> dict:
+    """Physical cores, hardware threads usable by this process and the CPU
+    model of this host (from /proc/cpuinfo and the affinity mask)."""
+    cores, model = set(), None
+    phys = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if ":" not in line:
+                continue
+            key, val = (s.strip() for s in line.split(":", 1))
+            if key == "model name" and model is None:
+                model = val
+            elif key == "physical id":
+                phys = val
+            elif key == "core id":
+                cores.add((phys, val))
+    except OSError:
+        pass
+    try:
+        threads = len(os.sched_getaffinity(0))
+    except AttributeError:
+        threads = os.cpu_count() or 1
+    return {"physical_cores": len(cores) or None, "threads": threads, "cpu_model": model}

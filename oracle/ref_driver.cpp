@@ -19,11 +19,15 @@
 //   ref_gen_paper   -> the loop of bench::gen_paper_matrices (bench.cpp:278-292)
 //   ref_renorm5 / ref_vseb / ref_two_* -> mpfkit::eft (eft.hpp)
 //   ref_op_counts   -> linalg::op_counters_read (linalg.cpp:13-25)
+//   ref_prep_*      -> matmul_block_parallel_into on operands built once,
+//                      timed inside C++ (the reported CPU baseline)
 // Errors: reference exceptions become a nonzero return and a message in
 // ref_last_error().
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 #include <thread>
 
@@ -137,6 +141,43 @@ void binop_w(int op, const double* x, const double* y, double* r) {
   for (int w = 0; w < W; ++w) r[w] = c.c[w];
 }
 
+
+// ---- prepared operands for the timed CPU baseline (bench.py --impl reference)
+// The reference MPMatrix objects are built ONCE (outside any timing); each
+// ref_prep_run() then times exactly one mpfkit::linalg::
+// matmul_block_parallel_into call (linalg.hpp:402-433) with steady_clock,
+// the way bench::time_matmul times its repetitions (bench.cpp:33-38).
+struct PrepBase {
+  virtual ~PrepBase() = default;
+  virtual void run(std::size_t n_min, int variant, unsigned workers) = 0;
+  virtual void result(double* C, std::size_t ldc) const = 0;
+  virtual PrepBase* with_a(std::size_t m, const double* A, std::size_t lda) const = 0;
+};
+
+template <int W>
+struct Prep final : PrepBase {
+  linalg::MPMatrix<W> a;
+  std::shared_ptr<const linalg::MPMatrix<W>> b;  // shared by handles made with with_a()
+  linalg::MPMatrix<W> c;
+  Prep(std::size_t m, std::size_t K, const double* A, std::size_t lda,
+       std::shared_ptr<const linalg::MPMatrix<W>> bm)
+      : a(load<W>(A, m, K, lda)), b(std::move(bm)), c(m, b->cols()) {}
+  void run(std::size_t n_min, int variant, unsigned workers) override {
+    linalg::matmul_block_parallel_into(c, a, *b, n_min, static_cast<linalg::KernelVariant>(variant),
+                                       workers);
+  }
+  void result(double* C, std::size_t ldc) const override { store<W>(c, C, ldc); }
+  PrepBase* with_a(std::size_t m, const double* A, std::size_t lda) const override {
+    return new Prep<W>(m, b->rows(), A, lda, b);
+  }
+};
+
+template <int W>
+PrepBase* new_prep(std::size_t m, std::size_t K, std::size_t n, const double* A, std::size_t lda,
+                   const double* B, std::size_t ldb) {
+  auto bm = std::make_shared<const linalg::MPMatrix<W>>(load<W>(B, K, n, ldb));
+  return new Prep<W>(m, K, A, lda, std::move(bm));
+}
 }  // namespace
 
 extern "C" {
@@ -318,5 +359,44 @@ void ref_random_normalized(int W, std::uint64_t* state, int is_signed, double* o
   }
   *state = g.state;
 }
+
+
+// Build the reference matrices for C(m x n) = A(m x K) * B(K x n) once.
+// Returns an opaque handle (null on error, message in ref_last_error()).
+void* ref_prep_new(int W, std::size_t m, std::size_t K, std::size_t n, const double* A,
+                   std::size_t lda, const double* B, std::size_t ldb) {
+  PrepBase* p = nullptr;
+  const int rc = guarded([&] {
+    if (W == 2) p = new_prep<2>(m, K, n, A, lda, B, ldb);
+    else if (W == 3) p = new_prep<3>(m, K, n, A, lda, B, ldb);
+    else if (W == 4) p = new_prep<4>(m, K, n, A, lda, B, ldb);
+    else throw std::invalid_argument("bad width");
+  });
+  return rc ? nullptr : p;
+}
+
+// Another handle over the same (shared, not copied) B with a new m-row A.
+void* ref_prep_with_a(void* h, std::size_t m, const double* A, std::size_t lda) {
+  PrepBase* p = nullptr;
+  const int rc = guarded([&] { p = static_cast<PrepBase*>(h)->with_a(m, A, lda); });
+  return rc ? nullptr : p;
+}
+
+// One timed matmul_block_parallel_into on the prepared operands; the wall
+// seconds of that call alone go to *seconds.
+int ref_prep_run(void* h, std::size_t n_min, int variant, unsigned workers, double* seconds) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    static_cast<PrepBase*>(h)->run(n_min, variant, workers);
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+  });
+}
+
+void ref_prep_result(void* h, double* C, std::size_t ldc) {
+  static_cast<PrepBase*>(h)->result(C, ldc);
+}
+
+void ref_prep_free(void* h) { delete static_cast<PrepBase*>(h); }
 
 }  // extern "C"

@@ -96,6 +96,9 @@ _SIGS = {
     "mpfk_gemm_device_gathered": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                             _U64, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_U64), _U64, _P,
                                             C.POINTER(C.c_int)]),
+    "mpfk_gemm_device_staged": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
+                                          _U64, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_U64), _U64, _P,
+                                          C.POINTER(C.c_int)]),
     "mpfk_device_alloc": (C.c_int, [_U64, C.POINTER(C.c_void_p)]),
     "mpfk_device_free": (C.c_int, [_P]),
     "mpfk_memcpy": (C.c_int, [_P, _P, _U64]),

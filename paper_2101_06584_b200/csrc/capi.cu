@@ -109,6 +109,7 @@ __global__ void selftest_kernel(const double* in, int* ok) {
 }
 
 constexpr int kMaxChunks = 16;  // row chunks / K panels of a host-buffer GEMM
+constexpr int kStagedPanels = 8;  // K panels of mpfk_gemm_device_staged
 
 #include "host_stage.inl"
 
@@ -133,6 +134,7 @@ struct Device {
   size_t gate_cap = 0;
   cudaStream_t gather = nullptr;   // copy-engine all-gather of B (mpfk_gemm_device_gathered)
   cudaEvent_t evG[3] = {};         // gate reset, gather done, last use of ggate finished
+  cudaEvent_t evS[kStagedPanels + 1] = {};  // mpfk_gemm_device_staged: start, K panel p gathered
   unsigned* ggate = nullptr;       // its flags/counters (cudaMalloc'd: stream memory operations
   size_t ggate_cap = 0;            // reject stream-ordered pool memory)
   Stager stage;  // pageable host operands
@@ -253,6 +255,7 @@ void ensure_devices(int n, int first = 0) {
     ck(cudaStreamCreateWithFlags(&D.stream2, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&D.gather, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : D.evG) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    for (auto& e : D.evS) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     for (auto& e : D.evB) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&D.evJ, cudaEventDisableTiming), "cudaEventCreate");
     for (auto& e : D.ev) ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -908,13 +911,20 @@ int mpfk_init(int n_gpus) {
 }
 
 void mpfk_shutdown(void) {
+  // the same lock order as the calls (host call, gather, table): no host
+  // GEMM, gathered/staged GEMM or table change can be in flight
+  std::lock_guard<std::mutex> call_lock(g_call_mu);
+  std::vector<std::unique_lock<std::mutex>> gather_locks;
+  for (auto& m : g_gather_mu) gather_locks.emplace_back(m);
   std::lock_guard<std::mutex> lk(g_mu);
   int prev = 0;
   cudaGetDevice(&prev);
   for (auto& D : g_dev) {
     if (!D.ready) continue;
     cudaSetDevice(D.id);
-    cudaStreamSynchronize(D.stream);
+    // every library stream (compute, copies, gather) and whatever the
+    // device-resident entry points queued on callers' streams
+    cudaDeviceSynchronize();
     if (D.dA) cudaFree(D.dA);
     if (D.dB) cudaFree(D.dB);
     if (D.dC) cudaFree(D.dC);
@@ -929,6 +939,7 @@ void mpfk_shutdown(void) {
     cudaStreamDestroy(D.stream2);
     cudaStreamDestroy(D.gather);
     for (auto& e : D.evG) cudaEventDestroy(e);
+    for (auto& e : D.evS) cudaEventDestroy(e);
     for (auto& e : D.evB) cudaEventDestroy(e);
     cudaEventDestroy(D.evJ);
     D.stage.release();
@@ -1293,57 +1304,113 @@ int mpfk_gemm_device_pull(int width, uint64_t m, uint64_t n, uint64_t k, const d
   });
 }
 
+
+// ---------------------------------------------------------------------------
+// B row-sliced across devices (the all-gather -> GEMM entry points)
+// ---------------------------------------------------------------------------
+// Rows [row0[s], row0[s+1]) of B live in slice s, a W-plane (rows_s x ldb)
+// array on this device, a peer device, or CUDA-IPC-mapped peer memory.
+struct Slices {
+  int n;
+  const double* const* src;
+  const uint64_t* row0;
+  std::vector<char> local;  // slice is on this device (or of unknown placement)
+  bool remote_on_copy_engines = true;  // every remote slice is on a P2P-capable peer
+
+  Slices(int nsrc, const double* const* s, const uint64_t* r, uint64_t k, int max_src, int dev_id)
+      : n(nsrc), src(s), row0(r), local(nsrc, 0) {
+    if (nsrc < 1 || nsrc > max_src) fail(MPFK_EINVAL, "mpfk: 1.." + std::to_string(max_src) + " source slices");
+    if (!s || !r) fail(MPFK_EINVAL, "mpfk: null source table");
+    if (r[0] != 0 || r[nsrc] != k) fail(MPFK_EINVAL, "mpfk: source slices must cover rows [0, k)");
+    for (int i = 0; i < nsrc; ++i)
+      if (r[i + 1] < r[i]) fail(MPFK_EINVAL, "mpfk: source slices out of order");
+    for (int i = 0; i < nsrc; ++i) {
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, s[i]) != cudaSuccess) {
+        cudaGetLastError();
+        local[i] = 1;  // unknown: the safe side
+        continue;
+      }
+      local[i] = at.type != cudaMemoryTypeDevice || at.device == dev_id;
+      if (!local[i]) {
+        // a peer copy runs on the copy engines only over a P2P path; without
+        // one the driver stages it, possibly with copy kernels that a GEMM
+        // waiting inside the kernel for the data would starve
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, dev_id, at.device) != cudaSuccess) cudaGetLastError(), can = 0;
+        if (!can) remote_on_copy_engines = false;
+      }
+    }
+  }
+
+  // rows [k0, k1) of B from the slices that hold them into B (whole rows of
+  // ldb doubles per plane) on stream cs; which: 1 local slices, 0 remote, -1 all
+  void copy(int W, double* B, uint64_t ldb, uint64_t b_plane, uint64_t k0, uint64_t k1, cudaStream_t cs,
+            int which) const {
+    for (int i = 0; i < n; ++i) {
+      if (which >= 0 && local[i] != which) continue;
+      const uint64_t a = std::max(k0, row0[i]), b = std::min(k1, row0[i + 1]);
+      if (a >= b) continue;
+      const uint64_t rows_s = row0[i + 1] - row0[i];
+      for (int w = 0; w < W; ++w)
+        ck(cudaMemcpyAsync(B + w * b_plane + a * ldb, src[i] + w * rows_s * ldb + (a - row0[i]) * ldb,
+                           sizeof(double) * (b - a) * ldb, cudaMemcpyDefault, cs),
+           "gather copy");
+    }
+  }
+};
+
+static void check_device_operands(uint64_t n, uint64_t k, const double* A, uint64_t lda, uint64_t a_plane,
+                           const double* B, uint64_t ldb, uint64_t b_plane, const double* C, uint64_t ldc,
+                           uint64_t c_plane) {
+  if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
+  if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
+    fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+    fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+}
+
+// K panel boundaries of the staged all-gather -> GEMM: a short first panel
+// (its gather is the only exposed transfer), each next panel 4x the last,
+// so every panel's compute covers the gather of the next; the last panel
+// runs to k.  head_rows overrides the first panel's height.
+static std::vector<uint64_t> staged_panels(uint64_t k, uint64_t head_rows) {
+  std::vector<uint64_t> cut{0};
+  uint64_t h = head_rows ? head_rows : 64;
+  h = std::max<uint64_t>(16, (h + 15) / 16 * 16);
+  while ((int)cut.size() < kStagedPanels && cut.back() + h < k && h * 2 <= k - cut.back()) {
+    cut.push_back(cut.back() + h);
+    h *= 4;
+  }
+  cut.push_back(k);
+  return cut;
+}
+
 int mpfk_gemm_device_gathered(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
                               uint64_t a_plane, double* B, uint64_t ldb, uint64_t b_plane, double* C, uint64_t ldc,
                               uint64_t c_plane, int nsrc, const double* const* src, const uint64_t* src_row0,
                               uint64_t panel_rows, void* stream, int* launches) {
   return guarded([&] {
     check_width(width);
-    if (nsrc < 1 || nsrc > 64) fail(MPFK_EINVAL, "mpfk: 1..64 source slices");
-    if (!src || !src_row0) fail(MPFK_EINVAL, "mpfk: null source table");
-    if (src_row0[0] != 0 || src_row0[nsrc] != k) fail(MPFK_EINVAL, "mpfk: source slices must cover rows [0, k)");
-    for (int s_ = 0; s_ < nsrc; ++s_)
-      if (src_row0[s_ + 1] < src_row0[s_]) fail(MPFK_EINVAL, "mpfk: source slices out of order");
     if (panel_rows < 16 || panel_rows % 16) fail(MPFK_EINVAL, "mpfk: panel_rows must be a positive multiple of 16");
-    if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
-    if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
-      fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
-    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
-      fail(MPFK_EINVAL, "mpfk: device operands must be 16-byte aligned");
+    check_device_operands(n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane);
     const int dev = current_device();
     ensure_devices(1, dev);
     Device& D = g_dev[dev];
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // panel p of B = rows [p*panel_rows, ...) gathered from the slices that
-    // hold them, whole rows of ldb doubles per plane
-    // A slice on this very device is copied in stream order BEFORE the GEMM:
-    // device-local copies may run as copy kernels, which a GEMM that fills
-    // every SM slot while it waits on panel flags would starve.  Slices on
-    // other GPUs move over NVLink on the copy engines, concurrently.
-    std::vector<char> local(nsrc, 0);
-    for (int s_ = 0; s_ < nsrc; ++s_) {
-      cudaPointerAttributes at;
-      if (cudaPointerGetAttributes(&at, src[s_]) != cudaSuccess) {
-        cudaGetLastError();
-        local[s_] = 1;  // unknown: the safe side
-      } else {
-        local[s_] = at.type != cudaMemoryTypeDevice || at.device == g_dev[dev].id;
-      }
-    }
-    auto copy_panel = [&](uint64_t k0, uint64_t k1, cudaStream_t cs, int which) {  // which: 1 local, 0 remote, -1 all
-      for (int s_ = 0; s_ < nsrc; ++s_) {
-        if (which >= 0 && local[s_] != which) continue;
-        const uint64_t a = std::max(k0, src_row0[s_]), b = std::min(k1, src_row0[s_ + 1]);
-        if (a >= b) continue;
-        const uint64_t rows_s = src_row0[s_ + 1] - src_row0[s_];
-        for (int w = 0; w < width; ++w)
-          ck(cudaMemcpyAsync(B + w * b_plane + a * ldb, src[s_] + w * rows_s * ldb + (a - src_row0[s_]) * ldb,
-                             sizeof(double) * (b - a) * ldb, cudaMemcpyDefault, cs),
-             "gather copy");
-      }
+    // hold them.  A slice on this very device is copied in stream order
+    // BEFORE the GEMM: device-local copies may run as copy kernels, which a
+    // GEMM that fills every SM slot while it waits on panel flags would
+    // starve.  Slices on other GPUs move over NVLink on the copy engines,
+    // concurrently -- only when every such peer is P2P-reachable; otherwise
+    // (S.remote_on_copy_engines false) the whole gather precedes a plain GEMM.
+    const Slices S(nsrc, src, src_row0, k, 64, D.id);
+    auto copy_panel = [&](uint64_t k0, uint64_t k1, cudaStream_t cs, int which) {
+      S.copy(width, B, ldb, b_plane, k0, k1, cs, which);
     };
     int l = 0;
-    if (!(m && n && k) || !memops_available()) {
+    if (!(m && n && k) || !memops_available() || !S.remote_on_copy_engines) {
       // no stream memory operations: gather everything, then the plain GEMM
       if (m && n)
         for (uint64_t k0 = 0; k0 < k; k0 += panel_rows) copy_panel(k0, std::min(k, k0 + panel_rows), s, -1);
@@ -1391,6 +1458,52 @@ int mpfk_gemm_device_gathered(int width, uint64_t m, uint64_t n, uint64_t k, con
       l = 1;
       ck(cudaStreamWaitEvent(s, D.evG[1], 0), "join gather");  // B complete when the stream is
       ck(cudaEventRecord(D.evG[2], s), "event");
+    }
+    count_matmul(m, n, k);
+    if (launches) *launches = l;
+  });
+}
+
+
+int mpfk_gemm_device_staged(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                            uint64_t a_plane, double* B, uint64_t ldb, uint64_t b_plane, double* C, uint64_t ldc,
+                            uint64_t c_plane, int nsrc, const double* const* src, const uint64_t* src_row0,
+                            uint64_t head_rows, void* stream, int* launches) {
+  return guarded([&] {
+    check_width(width);
+    check_device_operands(n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane);
+    const int dev = current_device();
+    ensure_devices(1, dev);
+    Device& D = g_dev[dev];
+    const Slices S(nsrc, src, src_row0, k, 64, D.id);
+    for (int i = 0; i < nsrc; ++i)
+      if (reinterpret_cast<uintptr_t>(src[i]) & 15) fail(MPFK_EINVAL, "mpfk: source slices must be 16-byte aligned");
+    if (head_rows % 16) fail(MPFK_EINVAL, "mpfk: head_rows must be a multiple of 16 (0: automatic)");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int l = 0;
+    if (!(m && n && k)) {
+      if (n && k) S.copy(width, B, ldb, b_plane, 0, k, s, -1);
+      l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, s);
+    } else {
+      // the gather runs on the device's gather stream -- peer slices on the
+      // copy engines over NVLink -- in ascending K panels, one event per
+      // panel; panel p's GEMM launch (p > 0 continues the chains kept in C)
+      // waits for that event only.  No kernel ever waits on a flag, so the
+      // schedule cannot stall whatever engine the driver picks for a copy.
+      const std::vector<uint64_t> cut = staged_panels(k, head_rows);
+      const int np = (int)cut.size() - 1;
+      std::lock_guard<std::mutex> lk(g_gather_mu[dev % 64]);
+      ck(cudaEventRecord(D.evS[0], s), "event");  // B's buffer is free in stream order
+      ck(cudaStreamWaitEvent(D.gather, D.evS[0], 0), "wait stream");
+      for (int p = 0; p < np; ++p) {
+        S.copy(width, B, ldb, b_plane, cut[p], cut[p + 1], D.gather, -1);
+        ck(cudaEventRecord(D.evS[p + 1], D.gather), "event");
+      }
+      for (int p = 0; p < np; ++p) {
+        ck(cudaStreamWaitEvent(s, D.evS[p + 1], 0), "wait panel");
+        l += enqueue_gemm(width, m, n, cut[p + 1] - cut[p], A + cut[p], lda, a_plane, B + cut[p] * ldb, ldb,
+                          b_plane, C, ldc, c_plane, s, p > 0);
+      }
     }
     count_matmul(m, n, k);
     if (launches) *launches = l;

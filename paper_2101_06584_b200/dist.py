@@ -292,8 +292,10 @@ class PeerBSlices:
             L.memcpy(self.local, a.ctypes.data, a.nbytes)
 
     def step(self, W, dA, dB, dC, rows, n, k, panel_rows=256, chunk_rows=2, stream=None, mode="pull") -> int:
-        """C_shard = A_shard * B with B gathered from the slices while ONE GEMM
-        launch computes: mode "copy" -- the copy engines copy B's panels and
+        """C_shard = A_shard * B with B gathered from the slices while the GEMM
+        computes: mode "staged" -- the copy engines gather B in growing K
+        panels and one GEMM launch per panel waits on that panel's event
+        (mpfk_gemm_device_staged); mode "copy" -- the copy engines copy B's panels and
         flag them, the kernel waits per panel (mpfk_gemm_device_gathered);
         mode "pull" -- the GEMM's own CTAs pull the panels over peer memory
         (mpfk_gemm_device_pull)."""
@@ -302,12 +304,16 @@ class PeerBSlices:
             return 0
         s = stream.cuda_stream if stream is not None else 0
         lda, ldb, ldc = dA.shape[2], dB.shape[2], dC.shape[2]
+        if mode == "staged":
+            return L.gemm_device_staged(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
+                                        dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, self.ptrs,
+                                        self.cuts, 0, s)
         if mode == "copy":
             return L.gemm_device_gathered(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
                                           dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, self.ptrs,
                                           self.cuts, panel_rows, s)
         if mode != "pull":
-            raise ValueError("PeerBSlices.step: mode must be 'copy' or 'pull'")
+            raise ValueError("PeerBSlices.step: mode must be 'staged', 'copy' or 'pull'")
         return L.gemm_device_pull(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
                                   dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, self.ptrs, self.cuts,
                                   panel_rows, chunk_rows, s)

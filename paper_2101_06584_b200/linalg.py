@@ -79,6 +79,9 @@ class MPMatrix:
             nbytes = 8 * W * self._rows * self._stride
             self._owner = _Pinned(nbytes)
             buf = (C.c_double * (nbytes // 8)).from_address(self._owner.ptr)
+            # numpy's base chain (data -> buf) keeps the page-locked block alive
+            # for views that outlive this MPMatrix
+            buf._owner = self._owner
             self.data = np.frombuffer(buf, dtype=np.float64).reshape(shape)
             self.data[...] = 0.0
         else:
@@ -497,6 +500,22 @@ def gemm_device_gathered(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a
     N.check(N.lib().mpfk_gemm_device_gathered(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
                                               c_plane, ns, srcs, rows, panel_rows, stream or None,
                                               C.byref(launches)))
+    return launches.value
+
+
+def gemm_device_staged(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int,
+                       ldb: int, b_plane: int, C_ptr: int, ldc: int, c_plane: int, src_ptrs, src_row0,
+                       head_rows: int = 0, stream: int = 0) -> int:
+    """All-gather -> GEMM with the copy engines gathering B's K panels from
+    the source slices and one GEMM launch per panel gated on that panel's
+    event (mpfk_gemm_device_staged); B_ptr receives the whole B."""
+    ns = len(src_ptrs)
+    srcs = (C.c_void_p * ns)(*src_ptrs)
+    rows = (C.c_uint64 * (ns + 1))(*src_row0)
+    launches = C.c_int(0)
+    N.check(N.lib().mpfk_gemm_device_staged(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
+                                            c_plane, ns, srcs, rows, head_rows, stream or None,
+                                            C.byref(launches)))
     return launches.value
 
 

@@ -26,31 +26,55 @@ def _port():
 def test_torchrun_collective_path(gpu_lib, workload):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--workload", workload,
-           "--steps", "2", "--warmup", "1", "--no-e2e", "--no-cpu-baseline", "--dist", "--check", "--panels", "3"]
+           "--steps", "2", "--warmup", "1", "--no-e2e", "--no-cpu-baseline", "--dist", "--check", "--panels", "3",
+           "--extra", "none"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["check_sharded_equals_one_shot"] is True
     assert line["gpu_launches"] == 2 * 3  # 3 K panels per step
-    assert "K panels overlapped" in line["config"]["parallelism"] or line["n_gpus"] == 1
+    assert "K panels overlapped" in line["transport"]
+    assert line["comm"] == {"backend": "nccl", "nranks": 1}
+    assert len(line["per_rank_kernel_ms"]) == 1
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["copy", "pull"])
-def test_torchrun_fused_allgather_path(gpu_lib, mode):
-    """--fused-allgather with one rank: B gathered from the rank's slice
-    while one GEMM launch computes (copy engines + flags, or in-kernel
-    pulls); the result equals the one-shot GEMM."""
+@pytest.mark.parametrize("mode,launches", [("copy", 1), ("pull", 1), ("staged", 3)])
+def test_torchrun_fused_allgather_path(gpu_lib, mode, launches):
+    """B gathered from the rank's slice while the GEMM computes: copy
+    engines + in-kernel flags (copy), in-kernel pulls (pull), or copy
+    engines + one launch per growing K panel (staged: k=1024 -> panels
+    [0,64), [64,320), [320,1024)); the result equals the one-shot GEMM."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--workload", "td1024",
-           "--steps", "2", "--warmup", "1", "--no-e2e", "--no-cpu-baseline", "--dist", "--check",
-           "--fused-allgather", "--gather-mode", mode, "--pull-panel", "64", "--pull-chunk", "8"]
+           "--steps", "2", "--warmup", "1", "--no-e2e", "--no-cpu-baseline", "--dist",
+           "--transport", mode, "--pull-panel", "64", "--pull-chunk", "8", "--extra", "none"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
-    assert line["check_sharded_equals_one_shot"] is True
-    assert line["gpu_launches"] == 2
-    assert "fused all-gather" in line["config"]["parallelism"]
+    assert line["check_sharded_equals_one_shot"] is True  # the default with a process group
+    assert line["gpu_launches"] == 2 * launches
+    assert {"copy": "gathered", "pull": "device_pull", "staged": "device_staged"}[mode] in line["transport"]
+
+
+@pytest.mark.gpu
+def test_bench_line_carries_every_workload(gpu_lib):
+    """The default line's `workloads`: every BASELINE config besides the
+    headline, each with value, roofline (frac and frac_executed), pinned and
+    pageable e2e (bit-identical to the device run) and clocks."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--workload", "dd1024", "--extra",
+           "td1024,qd1024", "--steps", "2", "--warmup", "1", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["config"]["workload"] == "dd1024"
+    assert set(line["workloads"]) == {"td1024", "qd1024"}
+    for rec in [line] + list(line["workloads"].values()):
+        assert rec["value"] > 0
+        assert 0 < rec["roofline"]["frac_executed"] <= 1.02
+        assert rec["e2e"]["matches_device_run"] is True
+        assert rec["e2e_pageable"]["matches_device_run"] is True
+        assert rec["gpu_launches"] >= 2
 
 
 @pytest.mark.gpu
