@@ -81,7 +81,7 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-buffer e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-waves", type=int, default=3,
+    ap.add_argument("--cpu-waves", type=int, default=2,
                     help="CPU samples: waves of 32-row blocks per reference worker")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--transport", choices=TRANSPORTS, default=None,

@@ -303,6 +303,10 @@ int mpfk_eft_batch(int op, uint64_t count, const double *a, const double *b, dou
 /* ---- op counters (linalg.hpp:160-180, linalg.cpp:10-25) ----------------- */
 void mpfk_op_counters_reset(void);
 void mpfk_op_counters_read(uint64_t *adds, uint64_t *muls, uint64_t *leaf_multiplies);
+/* What the calling thread's last entry point call added to the counters
+ * above (exact for that call even when other threads count concurrently);
+ * the C++ shim forwards it to the caller's own op counters. */
+void mpfk_last_op_counts(uint64_t *adds, uint64_t *muls, uint64_t *leaf_multiplies);
 
 /* TD/QD GEMM kernels run each k-tile with branch-free common paths (QD:
  * renorm5 path A, eft.hpp:255-257; TD: renorm5 paths A/B, eft.hpp:255-260,

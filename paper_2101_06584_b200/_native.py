@@ -109,6 +109,7 @@ _SIGS = {
     "mpfk_binop_batch": (C.c_int, [C.c_int, C.c_int, _U64, _P, _P, _P]),
     "mpfk_op_counters_reset": (None, []),
     "mpfk_op_counters_read": (None, [C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)]),
+    "mpfk_last_op_counts": (None, [C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)]),
     "mpfk_host_alloc": (_P, [_U64]),
     "mpfk_host_free": (None, [_P]),
     "mpfk_fill_baseline": (C.c_int, [C.c_int, C.c_int, _U64, _U64, _U64, _U64, _U64, _P, C.c_int]),

@@ -64,8 +64,21 @@ void ck(cudaError_t e, const char* what) {
   }
 }
 
+// op counts of the calling thread's current (outermost) entry point call:
+// the C++ shim forwards them to the caller's own counters (mpfk_last_op_counts)
+thread_local uint64_t t_ops[3];  // adds, muls, leaf multiplies
+thread_local int t_depth = 0;
+
+struct CallScope {
+  CallScope() {
+    if (t_depth++ == 0) t_ops[0] = t_ops[1] = t_ops[2] = 0;
+  }
+  ~CallScope() { --t_depth; }
+};
+
 template <class F>
 int guarded(F&& f) {
+  CallScope scope;
   try {
     f();
     return MPFK_OK;
@@ -86,10 +99,23 @@ int guarded(F&& f) {
 // ---------------------------------------------------------------------------
 std::atomic<uint64_t> g_adds{0}, g_muls{0}, g_leaf{0};
 
+void tally_adds(uint64_t v) {
+  g_adds.fetch_add(v, std::memory_order_relaxed);
+  t_ops[0] += v;
+}
+void tally_muls(uint64_t v) {
+  g_muls.fetch_add(v, std::memory_order_relaxed);
+  t_ops[1] += v;
+}
+void tally_leaf(uint64_t v) {
+  g_leaf.fetch_add(v, std::memory_order_relaxed);
+  t_ops[2] += v;
+}
+
 void count_matmul(uint64_t m, uint64_t n, uint64_t k) {
   if (k == 0) return;
-  g_muls.fetch_add(m * n * k, std::memory_order_relaxed);
-  g_adds.fetch_add(m * n * (k - 1), std::memory_order_relaxed);
+  tally_muls(m * n * k);
+  tally_adds(m * n * (k - 1));
 }
 
 // ---------------------------------------------------------------------------
@@ -223,6 +249,13 @@ void run_selftest_current() {
   ck(cudaMemcpy(&ok, d_ok, sizeof ok, cudaMemcpyDeviceToHost), "selftest D2H");
   cudaFree(d_in);
   cudaFree(d_ok);
+  // testing hook: MPFK_SELFTEST_INJECT=rn|fma reports that probe as failed,
+  // so the error path (status MPFK_ERUNTIME -> std::runtime_error, as
+  // runtime.cpp:73-80 throws) can be exercised on a healthy GPU
+  if (const char* inj = std::getenv("MPFK_SELFTEST_INJECT")) {
+    if (!std::strcmp(inj, "rn")) ok &= ~1;
+    if (!std::strcmp(inj, "fma")) ok &= ~2;
+  }
   if (!(ok & 1))
     fail(MPFK_ERUNTIME,
          "mpfk: binary64 arithmetic is not rounding to nearest-even; "
@@ -699,7 +732,10 @@ int enqueue_ew(int W, int op, uint64_t rows, uint64_t cols, double* out, uint64_
 }
 
 void count_ew(int op, uint64_t rows, uint64_t cols) {  // linalg.hpp:682-683
-  (op == kern::EW_MUL ? g_muls : g_adds).fetch_add(rows * cols, std::memory_order_relaxed);
+  if (op == kern::EW_MUL)
+    tally_muls(rows * cols);
+  else
+    tally_adds(rows * cols);
 }
 
 void check_width(int W) {
@@ -1237,8 +1273,8 @@ int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const do
     const int l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane,
                                static_cast<cudaStream_t>(stream), true);
     if (k) {  // k more multiply-adds per element: k muls and k adds
-      g_muls.fetch_add(m * n * k, std::memory_order_relaxed);
-      g_adds.fetch_add(m * n * k, std::memory_order_relaxed);
+      tally_muls(m * n * k);
+      tally_adds(m * n * k);
     }
     if (launches) *launches = l;
   });
@@ -1675,6 +1711,12 @@ void mpfk_op_counters_read(uint64_t* adds, uint64_t* muls, uint64_t* leaf) {
   if (adds) *adds = g_adds.load(std::memory_order_relaxed);
   if (muls) *muls = g_muls.load(std::memory_order_relaxed);
   if (leaf) *leaf = g_leaf.load(std::memory_order_relaxed);
+}
+
+void mpfk_last_op_counts(uint64_t* adds, uint64_t* muls, uint64_t* leaf) {
+  if (adds) *adds = t_ops[0];
+  if (muls) *muls = t_ops[1];
+  if (leaf) *leaf = t_ops[2];
 }
 
 int mpfk_gemm_redo_count(uint64_t* count, int reset) {

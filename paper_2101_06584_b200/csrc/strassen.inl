@@ -78,7 +78,7 @@ struct StrassenCtx {
     // mat_add/mat_sub among the 7 (L: t in {0,1,4,5,6}; R: t in {0,2,3,5,6})
     uint64_t ops = 0;
     for (int t = t0; t < t1; ++t) ops += SIDE == 0 ? (t != 2 && t != 3) : (t != 1 && t != 4);
-    g_adds.fetch_add(ops * src.batch * h0 * h1, std::memory_order_relaxed);
+    tally_adds(ops * src.batch * h0 * h1);
   }
 
   void combine(const BMat& M, const BMat& C) {
@@ -92,7 +92,7 @@ struct StrassenCtx {
 #undef MPFK_CMB
     ck(cudaGetLastError(), "strassen combine launch");
     ++launches;
-    g_adds.fetch_add(8ull * C.batch * M.rows * M.cols, std::memory_order_relaxed);  // 8 adds/subs
+    tally_adds(8ull * C.batch * M.rows * M.cols);  // 8 adds/subs
   }
 
   // L: batch of m x K, R: batch of K x n; writes the products into C
@@ -101,12 +101,12 @@ struct StrassenCtx {
     const uint64_t m = L.rows, K = L.cols, n = R.cols;
     const int b = L.batch;
     if (std::min({m, K, n}) <= cutoff) {  // the leaves: one batched block GEMM
-      g_leaf.fetch_add(b, std::memory_order_relaxed);
+      tally_leaf(b);
       launches += enqueue_gemm_batched(W, b, m, n, K, L.p, L.ld, L.plane, L.bstride, R.p, R.ld, R.plane,
                                        R.bstride, C.p, C.ld, C.plane, C.bstride, s);
       if (K) {
-        g_muls.fetch_add(uint64_t(b) * m * n * K, std::memory_order_relaxed);
-        g_adds.fetch_add(uint64_t(b) * m * n * (K - 1), std::memory_order_relaxed);
+        tally_muls(uint64_t(b) * m * n * K);
+        tally_adds(uint64_t(b) * m * n * (K - 1));
       }
       return;
     }
@@ -152,7 +152,7 @@ int strassen_device(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, 
   b.p = const_cast<double*>(B), b.rows = k, b.cols = n, b.ld = ldb, b.plane = pb, b.bstride = W * pb, b.batch = 1;
   c.p = C, c.rows = m, c.cols = n, c.ld = ldc, c.plane = pc, c.bstride = W * pc, c.batch = 1;
   if (m == 0 || n == 0) {
-    g_leaf.fetch_add(1, std::memory_order_relaxed);  // min(m, K, n) <= cutoff: one empty leaf
+    tally_leaf(1);  // min(m, K, n) <= cutoff: one empty leaf
     return 0;
   }
   ctx.solve(a, b, c);
@@ -168,7 +168,7 @@ void host_strassen(int W, mpfk_mat* Cm, const mpfk_mat* A, const mpfk_mat* B, ui
   mpfk_stats st{};
   const uint64_t m = A->rows, K = A->cols, n = B->cols;
   if (m == 0 || n == 0) {
-    g_leaf.fetch_add(1, std::memory_order_relaxed);
+    tally_leaf(1);
     zero_host_pads(W, Cm);
     t_stats = st;
     return;
