@@ -133,6 +133,32 @@ const Entry kEntries[] = {
     EF(4, 32, 32, 16, 2, 2, 2, 1, 16, 2),
     E(3, 32, 32, 16, 2, 2, 2, 1, 16, 3),  // TD product
     E(4, 16, 32, 16, 1, 2, 2, 1, 16, 3),  // QD product
+    // round 2: tile widths of 28 so the tile count is a whole number of
+    // resident-CTA rounds on 148 SMs at n = 1024 (37 column tiles):
+    // DD 128x28 -> 296 tiles = 148 x 2 (one round at 2 CTAs/SM),
+    // 64x28 -> 592 = 148 x 4, 32x28 -> 1184 = 148 x 8
+    {2, "r2/2/128x28/4x4/ku16/mb2/fixk/onebar", run_cfg<TileCfg<2, 128, 28, 16, 4, 4, 2, 16, 16, 2, 1, 1>>,
+     info_cfg<TileCfg<2, 128, 28, 16, 4, 4, 2, 16, 16, 2, 1, 1>>},
+    {2, "r2/2/64x28/2x4/ku16/mb4/fixk/onebar", run_cfg<TileCfg<2, 64, 28, 16, 2, 4, 2, 16, 16, 4, 1, 1>>,
+     info_cfg<TileCfg<2, 64, 28, 16, 2, 4, 2, 16, 16, 4, 1, 1>>},
+    {2, "r2/2/64x28/4x2/ku16/mb4/fixk/onebar", run_cfg<TileCfg<2, 64, 28, 16, 4, 2, 2, 16, 16, 4, 1, 1>>,
+     info_cfg<TileCfg<2, 64, 28, 16, 4, 2, 2, 16, 16, 4, 1, 1>>},
+    {2, "r2/2/32x28/2x2/ku16/mb4/fixk/onebar", run_cfg<TileCfg<2, 32, 28, 16, 2, 2, 2, 16, 16, 4, 1, 1>>,
+     info_cfg<TileCfg<2, 32, 28, 16, 2, 2, 2, 16, 16, 4, 1, 1>>},
+    {2, "r2/2/64x56/4x4/ku16/mb2/fixk/onebar", run_cfg<TileCfg<2, 64, 56, 16, 4, 4, 2, 16, 16, 2, 1, 1>>,
+     info_cfg<TileCfg<2, 64, 56, 16, 4, 4, 2, 16, 16, 2, 1, 1>>},
+    {3, "r2/3/32x28/2x2/mb2/fastr1/vsebf", run_cfg<TileCfg<3, 32, 28, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 28, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1>>},
+    {3, "r2/3/64x28/2x2/mb1/fastr1/vsebf", run_cfg<TileCfg<3, 64, 28, 16, 2, 2, 2, 1, 16, 1, 0, 0, 1, 1>>,
+     info_cfg<TileCfg<3, 64, 28, 16, 2, 2, 2, 1, 16, 1, 0, 0, 1, 1>>},
+    {3, "r2/3/32x32/2x2/mb2/fastr1/vsebf(product)", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1>>},
+    {4, "r2/4/32x28/2x2/ku4/mb2/fixk/onebar/fastr2", run_cfg<TileCfg<4, 32, 28, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>>,
+     info_cfg<TileCfg<4, 32, 28, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>>},
+    {4, "r2/4/64x28/2x2/ku4/mb1/fixk/onebar/fastr2", run_cfg<TileCfg<4, 64, 28, 16, 2, 2, 2, 4, 16, 1, 1, 1, 2>>,
+     info_cfg<TileCfg<4, 64, 28, 16, 2, 2, 2, 4, 16, 1, 1, 1, 2>>},
+    {4, "r2/4/32x32/2x2/ku4/mb2/fixk/onebar/fastr2(product)", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>>},
 };
 
 // Compute-only ceiling of a tile configuration: the product's mac_step on
