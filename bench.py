@@ -510,6 +510,8 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
         e2e = measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned=True, dC_host=dC_host)
         if not ctx.use_dist and not args.no_pageable:
             e2e_pg = measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned=False, dC_host=dC_host)
+            e2e_pg["registered"] = measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned=False,
+                                               dC_host=dC_host, register=True)
 
     # ---- CPU baseline: the reference's own GEMM on this host (rank 0, N == 1)
     cpu = None
@@ -591,15 +593,20 @@ def describe_transport(transport, ws, args, note):
     return s + (f" [{note}]" if note else "")
 
 
-def measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned, dC_host):
+def measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned, dC_host, register=False):
     """The metric through the public host-buffer API: every step copies the
-    step's operands from host memory, computes and reads C back."""
+    step's operands from host memory, computes and reads C back.
+    register: pageable operands with the library's opt-in registration
+    cache on (mpfk_host_register_cache): the first (warm-up) call page-locks
+    them, the timed calls reuse them."""
     import numpy as np
     torch, dist, P, args = ctx.torch, ctx.dist, ctx.P, ctx.args
     m = k = n
     Ah = P.fill_baseline(W, rows, k, SEED_A, wide=wide, row0=r0, pinned=pinned)
     Bh = P.fill_baseline(W, k, n, SEED_B, wide=wide, pinned=pinned)
     Ch = P.MPMatrix(W, rows, n, pinned=pinned)
+    if register:
+        P.host_register_cache(8 * W * (rows * k + k * n + rows * n) + (64 << 20))
     if ctx.use_dist:
         # one rank per GPU: each rank copies its A shard and 1/ws of B from
         # the host; B's panels are all-gathered over NVLink
@@ -630,10 +637,15 @@ def measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned, dC_host):
                   "matmul_block_parallel_into (C ABI, host buffers)"}
     if st is not None:
         out["ms_breakdown"] = {k_: round(st[k_], 3) for k_ in ("h2d_ms", "kernel_ms", "d2h_ms", "total_ms")}
+    if register:
+        out["host_memory"] = "pageable, page-locked on first use by the registration cache (opt-in)"
+        out["registered_entries"] = P.host_register_cache_stats()["entries"]
     if rows and dC_host is not None:
         # the e2e result equals the device-resident run (same inputs)
         out["matches_device_run"] = bool(
             (torch.from_numpy(np.ascontiguousarray(Ch.data)).view(torch.int64) == dC_host.view(torch.int64)).all())
+    if register:  # drop the registrations before the buffers are freed
+        P.host_register_cache(0)
     del Ah, Bh, Ch
     return out
 

@@ -322,6 +322,20 @@ int mpfk_gemm_redo_count(uint64_t *count, int reset);
  * bandwidth.  Replaces aligned_alloc(32, .) of linalg.hpp:115. */
 void *mpfk_host_alloc(uint64_t bytes);
 void mpfk_host_free(void *p);
+/* Page-locking of long-lived pageable operands (opt-in; default capacity 0,
+ * or MPFK_HOST_REGISTER_CACHE_MB from the environment): with a nonzero
+ * capacity, a pageable host operand of >= 1 MiB given to a host-buffer call
+ * (matmul_*, gemm, Strassen, ew) is cudaHostRegister'ed -- the whole
+ * MPMatrix buffer, W planes from its base -- and kept registered in a
+ * bounded LRU set, so later calls on the same buffer copy it by direct DMA
+ * (the page-locked paths) instead of through the staging ring.  The caller
+ * must drop a cached buffer (mpfk_host_unregister(base), or capacity 0 to
+ * empty the set) BEFORE freeing it: freed-and-reused memory must never stay
+ * registered.  A reference MPMatrix (aligned_alloc, linalg.hpp:115) is such
+ * an operand.  mpfk_shutdown empties the set. */
+int mpfk_host_register_cache(uint64_t capacity_bytes);
+int mpfk_host_register_cache_stats(uint64_t *capacity, uint64_t *used, uint64_t *entries);
+int mpfk_host_unregister(const void *base);
 
 /* ---- seeded inputs (random.hpp:17-75) --------------------- */
 /* The BASELINE.json configurations, generated row-parallel on the host:

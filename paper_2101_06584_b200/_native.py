@@ -109,6 +109,9 @@ _SIGS = {
     "mpfk_binop_batch": (C.c_int, [C.c_int, C.c_int, _U64, _P, _P, _P]),
     "mpfk_op_counters_reset": (None, []),
     "mpfk_op_counters_read": (None, [C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)]),
+    "mpfk_host_register_cache": (C.c_int, [_U64]),
+    "mpfk_host_register_cache_stats": (C.c_int, [C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)]),
+    "mpfk_host_unregister": (C.c_int, [_P]),
     "mpfk_last_op_counts": (None, [C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)]),
     "mpfk_host_alloc": (_P, [_U64]),
     "mpfk_host_free": (None, [_P]),

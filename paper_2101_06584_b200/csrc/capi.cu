@@ -983,6 +983,7 @@ void mpfk_shutdown(void) {
   }
   g_dev.clear();
   g_ndev = -1;
+  host_reg_cache().clear();
   cudaSetDevice(prev);
 }
 
@@ -1198,7 +1199,8 @@ int mpfk_ew_apply_into(int width, int op, mpfk_mat* out, const mpfk_mat* a, cons
       grow(D.dB, D.capB, sizeof(double) * width * ps);
       grow(D.dC, D.capC, sizeof(double) * width * ps);
       const uint64_t pa = plane_of(a), pb = plane_of(b), po = plane_of(out);
-      const bool a_pin = is_pinned(a->base), b_pin = is_pinned(b->base), o_pin = is_pinned(out->base);
+      const bool a_pin = host_operand_pinned(a->base, width, pa), b_pin = host_operand_pinned(b->base, width, pb),
+                 o_pin = host_operand_pinned(out->base, width, po);
       D.stage.reset();
       ck(cudaEventRecord(D.ev[0], D.stream), "event");
       for (int w = 0; w < width; ++w) {
@@ -1747,6 +1749,22 @@ void* mpfk_host_alloc(uint64_t bytes) {
 
 void mpfk_host_free(void* p) {
   if (p) cudaFreeHost(p);
+}
+
+int mpfk_host_register_cache(uint64_t bytes) {
+  return guarded([&] { host_reg_cache().set_capacity(bytes); });
+}
+
+int mpfk_host_register_cache_stats(uint64_t* capacity, uint64_t* used, uint64_t* entries) {
+  return guarded([&] {
+    if (capacity) *capacity = host_reg_cache().capacity();
+    if (used) *used = host_reg_cache().used();
+    if (entries) *entries = host_reg_cache().entries();
+  });
+}
+
+int mpfk_host_unregister(const void* base) {
+  return guarded([&] { host_reg_cache().unregister(base); });
 }
 
 int mpfk_fill_baseline(int width, int wide, uint64_t row0, uint64_t rows, uint64_t cols,

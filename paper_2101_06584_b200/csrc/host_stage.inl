@@ -16,6 +16,119 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// ---------------------------------------------------------------------------
+// page-locking long-lived caller buffers (opt-in): a bounded LRU set of
+// cudaHostRegister'ed ranges, keyed by the exact operand buffer (one
+// MPMatrix<W> allocation: W planes from its base).  A registered operand
+// takes the page-locked paths (direct DMA, the copy-engine-gated launch)
+// from its second call on.  The caller promises the buffers stay allocated
+// while cached: freeing registered memory and reallocating at the same
+// address would leave a stale registration, so a caller that frees an
+// operand first drops it (mpfk_host_unregister) or empties the cache
+// (mpfk_host_register_cache(0)).  Off by default; mpfk_shutdown empties it.
+// ---------------------------------------------------------------------------
+class HostRegCache {
+ public:
+  void set_capacity(size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu_);
+    cap_ = bytes;
+    while (used_ > cap_ && !ents_.empty()) evict_lru_locked();
+  }
+  size_t capacity() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return cap_;
+  }
+  // true when [p, p + bytes) is page-locked after the call (cached, or
+  // registered now); false leaves the operand on the staging path
+  bool ensure(const void* p, size_t bytes) {
+    if (!p || bytes < kMinBytes) return false;
+    std::lock_guard<std::mutex> lk(mu_);
+    if (!cap_ || bytes > cap_) return false;
+    const char* b = static_cast<const char*>(p);
+    for (auto& e : ents_)
+      if (b >= e.base && b + bytes <= e.base + e.bytes) {
+        e.last = ++tick_;
+        return true;
+      }
+    // ranges overlapping the new one cannot stay registered beside it
+    for (size_t i = 0; i < ents_.size();)
+      if (b < ents_[i].base + ents_[i].bytes && ents_[i].base < b + bytes)
+        drop_locked(i);
+      else
+        ++i;
+    while (used_ + bytes > cap_ && !ents_.empty()) evict_lru_locked();
+    if (cudaHostRegister(const_cast<char*>(b), bytes, cudaHostRegisterDefault) != cudaSuccess) {
+      cudaGetLastError();  // e.g. registered by the caller already: not ours to manage
+      return false;
+    }
+    ents_.push_back(Ent{b, bytes, ++tick_});
+    used_ += bytes;
+    return true;
+  }
+  void unregister(const void* p) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (size_t i = 0; i < ents_.size();)
+      if (ents_[i].base == p)
+        drop_locked(i);
+      else
+        ++i;
+  }
+  void clear() {
+    std::lock_guard<std::mutex> lk(mu_);
+    while (!ents_.empty()) drop_locked(ents_.size() - 1);
+  }
+  size_t used() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return used_;
+  }
+  size_t entries() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return ents_.size();
+  }
+
+ private:
+  static constexpr size_t kMinBytes = size_t(1) << 20;  // below: the staging ring is as fast
+  struct Ent {
+    const char* base;
+    size_t bytes;
+    uint64_t last;
+  };
+  void drop_locked(size_t i) {
+    cudaHostUnregister(const_cast<char*>(ents_[i].base));
+    cudaGetLastError();
+    used_ -= ents_[i].bytes;
+    ents_.erase(ents_.begin() + (long)i);
+  }
+  void evict_lru_locked() {
+    size_t lru = 0;
+    for (size_t i = 1; i < ents_.size(); ++i)
+      if (ents_[i].last < ents_[lru].last) lru = i;
+    drop_locked(lru);
+  }
+  std::mutex mu_;
+  std::vector<Ent> ents_;
+  size_t cap_ = 0, used_ = 0;
+  uint64_t tick_ = 0;
+};
+
+HostRegCache& host_reg_cache() {
+  static HostRegCache* c = [] {
+    auto* r = new HostRegCache;  // never destroyed: mpfk_shutdown empties it
+    if (const char* env = std::getenv("MPFK_HOST_REGISTER_CACHE_MB"))
+      r->set_capacity(size_t(std::max(0L, std::atol(env))) << 20);
+    return r;
+  }();
+  return *c;
+}
+
+// an operand buffer of W planes (plane stride in doubles) is page-locked,
+// registering it through the cache when that is enabled
+bool host_operand_pinned(const void* base, int W, uint64_t plane_stride) {
+  if (!base) return true;
+  if (is_pinned(base)) return true;
+  return host_reg_cache().ensure(base, sizeof(double) * size_t(W) * plane_stride);
+}
+
 // persistent workers running one job at a time: f(worker, workers)
 class CopyPool {
  public:

@@ -145,6 +145,22 @@ const Entry kEntries[] = {
      info_cfg<TileCfg<2, 64, 28, 16, 4, 2, 2, 16, 16, 4, 1, 1>>},
     {2, "r2/2/32x28/2x2/ku16/mb4/fixk/onebar", run_cfg<TileCfg<2, 32, 28, 16, 2, 2, 2, 16, 16, 4, 1, 1>>,
      info_cfg<TileCfg<2, 32, 28, 16, 2, 2, 2, 16, 16, 4, 1, 1>>},
+    // n = 1024 in ONE resident round: 1024 32x32 tiles on 148 SMs x 7 CTAs
+    // of 128 threads (2x4 / 4x2 micro-tiles; BK 8 so 7 CTAs fit in smem)
+    {2, "r2/2/32x32x8/2x4/ku8/mb7/fixk/onebar", run_cfg<TileCfg<2, 32, 32, 8, 2, 4, 2, 8, 16, 7, 1, 1>>,
+     info_cfg<TileCfg<2, 32, 32, 8, 2, 4, 2, 8, 16, 7, 1, 1>>},
+    {2, "r2/2/32x32x8/4x2/ku8/mb7/fixk/onebar", run_cfg<TileCfg<2, 32, 32, 8, 4, 2, 2, 8, 16, 7, 1, 1>>,
+     info_cfg<TileCfg<2, 32, 32, 8, 4, 2, 2, 8, 16, 7, 1, 1>>},
+    {2, "r2/2/32x32x8/2x4/ku8/mb8/fixk/onebar", run_cfg<TileCfg<2, 32, 32, 8, 2, 4, 2, 8, 16, 8, 1, 1>>,
+     info_cfg<TileCfg<2, 32, 32, 8, 2, 4, 2, 8, 16, 8, 1, 1>>},
+    {2, "r2/2/32x32x8/2x4/ku8/mb6/fixk/onebar", run_cfg<TileCfg<2, 32, 32, 8, 2, 4, 2, 8, 16, 6, 1, 1>>,
+     info_cfg<TileCfg<2, 32, 32, 8, 2, 4, 2, 8, 16, 6, 1, 1>>},
+    {2, "r2/2/32x32x8/2x2/ku8/mb4/fixk/onebar", run_cfg<TileCfg<2, 32, 32, 8, 2, 2, 2, 8, 16, 4, 1, 1>>,
+     info_cfg<TileCfg<2, 32, 32, 8, 2, 2, 2, 8, 16, 4, 1, 1>>},
+    {2, "r2/2/64x64/4x4/ku16/mb2/fixk/onebar(product)", run_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1>>,
+     info_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1>>},
+    {2, "r2/2/32x32/2x2/ku16/mb4/fixk/onebar(product)", run_cfg<TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1>>,
+     info_cfg<TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1>>},
     {2, "r2/2/64x56/4x4/ku16/mb2/fixk/onebar", run_cfg<TileCfg<2, 64, 56, 16, 4, 4, 2, 16, 16, 2, 1, 1>>,
      info_cfg<TileCfg<2, 64, 56, 16, 4, 4, 2, 16, 16, 2, 1, 1>>},
     {3, "r2/3/32x28/2x2/mb2/fastr1/vsebf", run_cfg<TileCfg<3, 32, 28, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1>>,

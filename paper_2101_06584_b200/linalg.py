@@ -337,6 +337,26 @@ def op_counters_read() -> OpCounts:
     return OpCounts(a.value, m.value, l_.value)
 
 
+def host_register_cache(capacity_bytes: int):
+    """Opt-in page-locking of long-lived pageable operands
+    (mpfk_host_register_cache): a bounded LRU set of registered MPMatrix
+    buffers; 0 disables and empties it.  Drop a buffer with
+    host_unregister() before freeing it."""
+    N.check(N.lib().mpfk_host_register_cache(int(capacity_bytes)))
+
+
+def host_register_cache_stats() -> dict:
+    cap, used, ents = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    N.check(N.lib().mpfk_host_register_cache_stats(C.byref(cap), C.byref(used), C.byref(ents)))
+    return {"capacity": cap.value, "used": used.value, "entries": ents.value}
+
+
+def host_unregister(m):
+    """Remove an MPMatrix (or a raw base address) from the registration cache."""
+    base = m.data.ctypes.data if isinstance(m, MPMatrix) else int(m)
+    N.check(N.lib().mpfk_host_unregister(base))
+
+
 def last_stats() -> dict:
     s = N.MpfkStats()
     N.check(N.lib().mpfk_last_stats(C.byref(s)))

@@ -5,6 +5,9 @@ ONE B200: rank 0's shard (rows shard_rows(m, N, 0) of C, full B) through
   * pull:  mpfk_gemm_device_pull with B split into N row slices that live in
            this GPU's own memory (the fused all-gather kernel's bookkeeping and
            copies, HBM-to-HBM instead of over NVLink),
+  * staged: mpfk_gemm_device_staged (bench.py's default transport) on the same
+           slices: copy-engine gather in growing K panels, one GEMM launch per
+           panel gated on its event (HBM-to-HBM copies here),
 
 and the projected strong-scaling efficiency T(1) / (N * T(N)).  Projection
 only: the NVLink leg is not exercised (each rank pulls (N-1)/N of B, DD n=8192
@@ -73,12 +76,22 @@ for N in (1, 2, 4, 8):
 
     tp = timed(pull)
     ok_pull = bool(torch.equal(Cp.view(torch.int64), ref[:, r0:r1].view(torch.int64)))
+    Cs = torch.zeros_like(Csh)
+    Bst = torch.zeros_like(B)
+
+    def staged():
+        P.gemm_device_staged(W, rows, n, n, Ash.data_ptr(), ld, rows * ld, Bst.data_ptr(), ld, n * ld,
+                             Cs.data_ptr(), ld, rows * ld, [x.data_ptr() for x in slices], cuts, 0, s.cuda_stream)
+
+    ts = timed(staged)
+    ok_staged = bool(torch.equal(Cs.view(torch.int64), ref[:, r0:r1].view(torch.int64)))
     if N == 1:
         t1 = plain
     macs = rows * n * n
     line = {"workload": a.workload, "ranks": N, "rows_per_rank": rows, "plain_ms": round(plain, 3),
-            "pull_ms": round(tp, 3), "bit_exact": ok_plain and ok_pull,
+            "pull_ms": round(tp, 3), "staged_ms": round(ts, 3), "bit_exact": ok_plain and ok_pull and ok_staged,
             "per_rank_frac_of_fp64_peak": round(macs * OPS_PER_MAC[W] / (plain * 1e-3) / P.fp64_peak()[0], 4),
             "projected_efficiency_plain": round(t1 / (N * plain), 4),
-            "projected_efficiency_pull": round(t1 / (N * tp), 4)}
+            "projected_efficiency_pull": round(t1 / (N * tp), 4),
+            "projected_efficiency_staged": round(t1 / (N * ts), 4)}
     print(json.dumps(line), flush=True)
