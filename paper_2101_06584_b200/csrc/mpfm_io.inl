@@ -65,7 +65,13 @@ MpfmHeader read_header(std::FILE* f, const std::string& path, int want_width) {
   if (r.width < 2 || r.width > 4) io_fail(path, "component width mismatch");
   if (std::fseek(f, 0, SEEK_END) != 0) io_fail(path, "cannot seek");
   const long long size = std::ftell(f);
-  const unsigned long long need = kMpfmHeader + 8ull * r.width * r.rows * r.stride;
+  // 33 + 8 W rows stride without wrapping: a crafted header must not pass
+  // the size check with an undersized payload
+  unsigned long long cells = 0, need = 0;
+  if (__builtin_mul_overflow((unsigned long long)r.rows, (unsigned long long)r.stride, &cells) ||
+      __builtin_mul_overflow(cells, 8ull * r.width, &need) ||
+      __builtin_add_overflow(need, (unsigned long long)kMpfmHeader, &need))
+    io_fail(path, "implausible dimensions");
   if (size < 0 || (unsigned long long)size < need) io_fail(path, "truncated");
   if ((unsigned long long)size > need) io_fail(path, "trailing data");
   std::fseek(f, (long)kMpfmHeader, SEEK_SET);
@@ -143,7 +149,9 @@ void mpfm_load(const char* cpath, int W, double* dst, uint64_t ld, uint64_t plan
   if (!F.f) io_fail(path, "cannot open");
   const MpfmHeader h = read_header(F.f, path, W);
   if (ld < h.cols) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
-  if (plane < h.rows * ld && h.rows) fail(MPFK_EINVAL, "mpfk: plane stride too small");
+  uint64_t plane_need = 0;
+  if (h.rows && (__builtin_mul_overflow(h.rows, ld, &plane_need) || plane < plane_need))
+    fail(MPFK_EINVAL, "mpfk: plane stride too small");
   if (h.rows == 0 || h.stride == 0) return;
   const uint64_t cr = chunk_rows(h.stride);
   Stage st(8 * std::min<uint64_t>(cr, h.rows) * h.stride, device);

@@ -48,6 +48,8 @@ def _write_raw(path, magic=b"MPFM", version=1, W=2, rows=2, cols=3, stride=None,
     (dict(version=2), "unsupported version"),
     (dict(W=3), "component width mismatch"),
     (dict(rows=2 ** 33, payload=b""), "implausible dimensions"),
+    # 8 W rows stride wraps 2^64 to 0: must not pass as a 33-byte file + payload
+    (dict(rows=2 ** 32, cols=2 ** 32, payload=b"\0" * 64), "implausible dimensions"),
     (dict(stride=5), "bad stride"),
     (dict(payload=b"\0" * 8), "truncated"),
     (dict(payload=b"\0" * (2 * 2 * 4 * 8 + 8)), "trailing data"),
