@@ -56,7 +56,7 @@ def _rank(rank, world, port, W, m, k, n, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["copy", "pull"])
+@pytest.mark.parametrize("mode", ["copy", "pull", "staged"])
 @pytest.mark.parametrize("W,m,k,n", [(2, 96, 200, 70), (4, 50, 131, 33)])
 def test_two_process_ipc_fused_allgather(gpu_lib, W, m, k, n, mode):
     import oracle as O
@@ -75,7 +75,8 @@ def test_two_process_ipc_fused_allgather(gpu_lib, W, m, k, n, mode):
     B = P.fill_baseline(W, k, n, 2, wide=True)
     want = O.ref_gemm(A.data, B.data, k, n)
     for rank, r0, r1, C, Bfull, launches in got:
-        assert launches == (1 if r1 > r0 else 0)
+        per = 2 if mode == "staged" else 1  # staged: K panels [0, 64), [64, k)
+        assert launches == (per if r1 > r0 else 0)
         assert np.array_equal(C.view(np.uint64), want[:, r0:r1].view(np.uint64))
         if r1 > r0:  # the pulled B is the whole matrix, bit for bit
             assert np.array_equal(Bfull.view(np.uint64), B.data.view(np.uint64))
