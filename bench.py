@@ -83,6 +83,7 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-waves", type=int, default=2,
                     help="CPU samples: waves of 32-row blocks per reference worker")
+    ap.add_argument("--cpu-steps", type=int, default=3, help="cpu_baseline: timed reference calls (median)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--transport", choices=TRANSPORTS, default=None,
                     help="N > 1 replication of B: staged (copy engines gather B's growing K panels from the "
@@ -268,8 +269,13 @@ def run_reference(args, n_gpus):
     """The reference arm: the reference's CPU GEMM, nothing of this repo's
     library on the path (only oracle/)."""
     ref = CpuReference(args.workload, waves=args.cpu_waves)
-    for _ in range(args.warmup):
-        ref.warmup()
+    for i in range(args.warmup):
+        # the first warm-up is the timed handle's own first call (its pages,
+        # its threads); the rest run the one-wave sample
+        if i == 0:
+            ref.step()
+        else:
+            ref.warmup()
     vals, secs = [], []
     for _ in range(args.steps):
         g, s = ref.step()
@@ -277,6 +283,7 @@ def run_reference(args, n_gpus):
         secs.append(s)
     ref.close()
     v = statistics.median(vals)
+    spread = [round(min(secs), 3), round(max(secs), 3)]
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -295,7 +302,9 @@ def run_reference(args, n_gpus):
         "cpu_baseline": ref.describe(v),
         "e2e": {"value": round(v, 4), "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    line["cpu_baseline"]["warmup_sample"] = f"{ref.warm_rows} rows (one wave) per warm-up step"
+    line["cpu_baseline"]["warmup_sample"] = (f"the timed sample once, then {ref.warm_rows} rows (one wave) per "
+                                             "further warm-up step")
+    line["cpu_baseline"]["step_seconds_min_max"] = spread
     emit(line, args)
 
 
@@ -519,8 +528,10 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
         try:
             ref = CpuReference(workload, waves=args.cpu_waves)
             ref.warmup()
-            g, _ = ref.step()
-            cpu = ref.describe(g)
+            ref.step()  # the timed handle's own first call, untimed
+            runs = [ref.step() for _ in range(max(1, args.cpu_steps))]
+            cpu = ref.describe(statistics.median(g for g, _ in runs))
+            cpu["step_seconds"] = [round(t, 3) for _, t in runs]
             ref.close()
         except Exception as e:  # the checker is optional; the GPU number stands alone
             cpu = {"value": None, "error": str(e)[:200]}
