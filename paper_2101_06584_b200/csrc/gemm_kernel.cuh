@@ -88,13 +88,18 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
+// 16 bytes, always valid (interior tiles): no src-size operand
+__device__ __forceinline__ void cp_async16_full(unsigned smem_addr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr), "l"(gmem));
+}
 
 // GROUP_M: tiles are visited in column-major order within bands of GROUP_M
 // tile rows, so the CTAs resident at one time cover a near-square block of C
 // and share their A and B panels in L2 instead of streaming all of B per
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
-          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0, int VSEBF_ = 0>
+          int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0, int VSEBF_ = 0,
+          int FLOAD_ = 1>
 struct TileCfg {
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
   static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
@@ -103,6 +108,9 @@ struct TileCfg {
   // slot of tile kt-1 (every warp is past it) and compute -- instead of
   // refill, wait, barrier, compute, barrier
   static constexpr int ONEBAR = ONEBAR_;
+  // interior tiles load full k-tiles with the precomputed-address loader
+  // (FastLoad); 0 keeps the general loader everywhere
+  static constexpr int FLOAD = FLOAD_;
   static constexpr int TX = BN / TN;  // threads along N
   static constexpr int TY = BM / TM;  // threads along M
   static constexpr int THREADS = TX * TY;
@@ -149,6 +157,72 @@ __device__ __forceinline__ void load_tile(double* As, double* Bs, const GemmArgs
     const double* src = ok ? g.B + w * g.pb + (long long)gk * g.ldb + gn : g.B;
     cp_async16(Bs + w * BK * Cfg::BS + r * Cfg::BS + 2 * nc, src, ok);
   }
+}
+
+// Interior-tile loader.  load_tile above is general (any edge, any k0) but
+// recomputes every chunk's (plane, row, column), bounds test and 64-bit
+// address per k-tile: ~30 instructions per 16-byte copy, ~5 % of a DD
+// thread's instruction stream next to its 5,120 FP64 instructions per
+// k-tile (profiles/r02: the non-FP64 share is what costs FP64 issue slots).
+// For a tile wholly inside M x N and a full k-tile, chunk `it` of a thread
+// sits at a fixed offset from the thread's first chunk -- whole planes and
+// whole row groups, since THREADS divides the chunks of a plane and is a
+// multiple of the chunks of a row -- so the copies reduce to one pointer
+// plus uniform offsets each, the pointers stepping by BK per k-tile.
+template <class Cfg>
+struct FastLoad {
+  static constexpr int T = Cfg::THREADS, BK = Cfg::BK, BM = Cfg::BM, BN = Cfg::BN;
+  static constexpr int ACH = BM * (BK / 2), BCH = BK * (BN / 2);
+  static constexpr bool ok =
+      Cfg::FLOAD && T % (BK / 2) == 0 && ACH % T == 0 && T % (BN / 2) == 0 && BCH % T == 0;
+  static constexpr int A_IT = ok ? ACH / T : 1;      // copies per plane of A
+  static constexpr int A_ROWS = ok ? T / (BK / 2) : 1;  // rows of A per copy round
+  static constexpr int B_IT = ok ? BCH / T : 1;
+  static constexpr int B_ROWS = ok ? T / (BN / 2) : 1;
+};
+
+struct FastLoadState {
+  const double* a;  // this thread's first A chunk at the current k-tile
+  const double* b;  // this thread's first B chunk at the current k-tile
+  unsigned sa, sb;  // their shared-memory offsets (bytes) within a stage
+};
+
+template <class Cfg>
+__device__ __forceinline__ FastLoadState fast_load_init(const GemmArgs& g, int m0, int n0, int k0) {
+  using F = FastLoad<Cfg>;
+  const int tid = threadIdx.x;
+  const int ra = tid / (Cfg::BK / 2), ka = 2 * (tid % (Cfg::BK / 2));
+  const int rb = tid / (Cfg::BN / 2), nb = 2 * (tid % (Cfg::BN / 2));
+  FastLoadState st;
+  st.a = g.A + (long long)(m0 + ra) * g.lda + k0 + ka;
+  st.b = g.B + (long long)(k0 + rb) * g.ldb + n0 + nb;
+  st.sa = 8u * (ra * Cfg::AS + ka);
+  st.sb = 8u * (rb * Cfg::BS + nb);
+  (void)sizeof(F);
+  return st;
+}
+
+// the k-tile the state points at into stage (As, Bs); then advance one k-tile
+template <class Cfg>
+__device__ __forceinline__ void fast_load_tile(FastLoadState& st, double* As, double* Bs, const GemmArgs& g) {
+  using F = FastLoad<Cfg>;
+  constexpr int W = Cfg::W;
+  const unsigned as = static_cast<unsigned>(__cvta_generic_to_shared(As)) + st.sa;
+  const unsigned bs = static_cast<unsigned>(__cvta_generic_to_shared(Bs)) + st.sb;
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+#pragma unroll
+    for (int it = 0; it < F::A_IT; ++it)
+      cp_async16_full(as + 8u * (w * Cfg::BM * Cfg::AS + it * F::A_ROWS * Cfg::AS),
+                      st.a + w * g.pa + (long long)(it * F::A_ROWS) * g.lda);
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+#pragma unroll
+    for (int it = 0; it < F::B_IT; ++it)
+      cp_async16_full(bs + 8u * (w * Cfg::BK * Cfg::BS + it * F::B_ROWS * Cfg::BS),
+                      st.b + w * g.pb + (long long)(it * F::B_ROWS) * g.ldb);
+  st.a += Cfg::BK;
+  st.b += (long long)Cfg::BK * g.ldb;
 }
 
 // linear CTA index -> (tile row, tile col) with GROUP_M-row bands
@@ -362,6 +436,12 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
       }
   }
 
+  // interior tile: every full k-tile takes the fast loader (FastLoad)
+  const bool interior = FastLoad<Cfg>::ok && m0 + BM <= g.M && n0 + Cfg::BN <= g.N;
+  const int kfull = g.K / BK;  // k-tiles [0, kfull) are full
+  FastLoadState fl{};
+  if (interior) fl = fast_load_init<Cfg>(g, m0, n0, 0);
+
   int ready_panel = -1;  // kPull: panels [0, ready_panel] are resident (visited in order)
   if (kGate && min(m0 + BM, g.M) > G.a_rows_first) wait_flag(G.a_rest);  // rows uploaded after the panels
 
@@ -378,7 +458,10 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
         ready_panel = s * BK / G.panel_rows;
         wait_flag(G.flags + ready_panel);
       }
-      load_tile<Cfg>(As0 + s * Cfg::A_STAGE, Bs0 + s * Cfg::B_STAGE, g, m0, n0, s * BK);
+      if (interior && s < kfull)
+        fast_load_tile<Cfg>(fl, As0 + s * Cfg::A_STAGE, Bs0 + s * Cfg::B_STAGE, g);
+      else
+        load_tile<Cfg>(As0 + s * Cfg::A_STAGE, Bs0 + s * Cfg::B_STAGE, g, m0, n0, s * BK);
     }
     cp_async_commit();
   }
@@ -402,7 +485,10 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
           ready_panel = nt * BK / G.panel_rows;
           wait_flag(G.flags + ready_panel);
         }
-        load_tile<Cfg>(As0 + slot * Cfg::A_STAGE, Bs0 + slot * Cfg::B_STAGE, g, m0, n0, nt * BK);
+        if (interior && nt < kfull)
+          fast_load_tile<Cfg>(fl, As0 + slot * Cfg::A_STAGE, Bs0 + slot * Cfg::B_STAGE, g);
+        else
+          load_tile<Cfg>(As0 + slot * Cfg::A_STAGE, Bs0 + slot * Cfg::B_STAGE, g, m0, n0, nt * BK);
       }
       cp_async_commit();
     }
