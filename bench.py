@@ -99,6 +99,10 @@ def parse(argv=None):
     ap.add_argument("--check", dest="check", action="store_true", default=None,
                     help="check the sharded step's C bitwise against a one-shot GEMM (default at N > 1)")
     ap.add_argument("--no-check", dest="check", action="store_false")
+    ap.add_argument("--emulate-on-one-gpu", action="store_true",
+                    help="TEST ONLY: run the N ranks on GPU 0 with a gloo group (the full N > 1 code path -- "
+                         "launcher, IPC slices, staged gather, sharded check -- on a one-GPU box; timings "
+                         "are meaningless, no e2e leg)")
     # round-1 spellings of --transport
     ap.add_argument("--no-overlap", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--nccl-bcast", action="store_true", help=argparse.SUPPRESS)
@@ -330,15 +334,25 @@ class Ctx:
         import paper_2101_06584_b200 as P
         self.args, self.ws, self.rank, self.local = args, ws, rank, local
         self.torch, self.dist, self.P = torch, dist, P
-        torch.cuda.set_device(local)
-        P.set_device(local)  # libmpfk has its own CUDA runtime: mirror the choice
-        self.dev = torch.device("cuda", local)
+        self.emulate = bool(args.emulate_on_one_gpu)
+        dev_index = 0 if self.emulate else local
+        torch.cuda.set_device(dev_index)
+        P.set_device(dev_index)  # libmpfk has its own CUDA runtime: mirror the choice
+        self.dev = torch.device("cuda", dev_index)
         self.use_dist = ws > 1 or args.dist
         if self.use_dist and not dist.is_initialized():
-            dist.init_process_group("nccl", device_id=self.dev)
+            if self.emulate:  # NCCL refuses two ranks on one device
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
+        # collectives of the bench's own bookkeeping (timings, flags): host
+        # tensors under gloo
+        self.coll_dev = torch.device("cpu") if self.emulate else self.dev
         self.transport = args.transport or ("staged" if ws > 1 else ("nccl" if self.use_dist else None))
         if self.transport == "pull" and ws > 8:
             raise SystemExit("bench: the pull transport maps at most 8 peer slices; use --transport staged")
+        if self.emulate and self.transport not in ("staged", "pull", "copy"):
+            raise SystemExit("bench: --emulate-on-one-gpu runs the peer-slice transports only")
         if not self.use_dist:
             self.transport = None
         self.stream = torch.cuda.current_stream(self.dev)
@@ -347,8 +361,9 @@ class Ctx:
         if self.use_dist:
             self.comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size()}
             if rank == 0:
-                print(f"bench: NCCL communicator nranks={self.comm['nranks']} backend={self.comm['backend']} "
-                      f"transport={self.transport}", file=sys.stderr, flush=True)
+                print(f"bench: {'NCCL' if self.comm['backend'] == 'nccl' else 'process-group'} communicator "
+                      f"nranks={self.comm['nranks']} backend={self.comm['backend']} transport={self.transport}",
+                      file=sys.stderr, flush=True)
 
     def barrier(self):
         if self.use_dist:
@@ -357,14 +372,21 @@ class Ctx:
     def max_over_ranks(self, vals):
         if not self.use_dist:
             return list(vals)
-        t = self.torch.tensor(list(vals), dtype=self.torch.float64, device=self.dev)
+        t = self.torch.tensor(list(vals), dtype=self.torch.float64, device=self.coll_dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return t.tolist()
+
+    def min_int(self, v):
+        if not self.use_dist:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.int32, device=self.coll_dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        return int(t.item())
 
     def gather_float(self, v):
         if not self.use_dist:
             return [v]
-        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.coll_dev)
         out = [self.torch.zeros_like(t) for _ in range(self.ws)]
         self.dist.all_gather(out, t)
         return [x.item() for x in out]
@@ -407,9 +429,7 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
             ok = 0
             note = f"peer slices unavailable ({type(e).__name__}: {str(e)[:120]})"
             print(f"bench: {note}; using the NCCL K-panel broadcast", file=sys.stderr)
-        t = torch.tensor([ok], dtype=torch.int32, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        if not int(t.item()):
+        if not ctx.min_int(ok):
             if slices is not None:
                 slices.close()
             slices = None
@@ -460,7 +480,7 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
     if ctx.peak_ops is None:
         ctx.peak_ops, _ = P.fp64_peak()  # FP64 pipe peak on this GPU (the roofline denominator)
 
-    clocks = ClockSampler(ctx.local)
+    clocks = ClockSampler(ctx.dev.index)
     ctx.barrier()
     torch.cuda.synchronize(dev)
     P.gemm_redo_count(reset=True)  # TD/QD fast-pass redo counter (synchronises; outside the timed region)
@@ -515,7 +535,7 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
 
     # ---- e2e through the public host-buffer API (C ABI)
     e2e = e2e_pg = None
-    if not args.no_e2e:
+    if not args.no_e2e and not ctx.emulate:
         e2e = measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned=True, dC_host=dC_host)
         if not ctx.use_dist and not args.no_pageable:
             e2e_pg = measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned=False, dC_host=dC_host)
@@ -698,6 +718,8 @@ def run_mpfk(args, ws, rank, local):
                 line[key] = head[key]
         if ctx.comm is not None:
             line["comm"] = ctx.comm
+        if ctx.emulate:
+            line["emulated_on_one_gpu"] = True  # a test of the N > 1 path, not a measurement
         if extras:
             line["workloads"] = extras
         emit(line, args)
@@ -717,7 +739,7 @@ def main(argv=None):
     from paper_2101_06584_b200 import launch
     if args.gpus is not None and args.gpus > 1 and not launch.under_launcher():
         try:
-            launch.require_devices(args.gpus)
+            launch.require_devices(1 if args.emulate_on_one_gpu else args.gpus)
         except RuntimeError as e:
             print(f"bench: {e}", file=sys.stderr)
             return 2
@@ -728,7 +750,7 @@ def main(argv=None):
         return 2
     if ws > 1:
         try:
-            launch.require_devices(ws)
+            launch.require_devices(1 if args.emulate_on_one_gpu else ws)
         except RuntimeError as e:
             print(f"bench: {e}", file=sys.stderr)
             return 2

@@ -115,3 +115,30 @@ def test_matmul_sharded_into_single_rank(gpu_lib, W, m, k, n, panels):
     assert launches == len(gather_panels(k, panels, 1)[1])
     with pytest.raises(ValueError, match="inner dimensions differ"):
         matmul_sharded_into(C1, A, P.MPMatrix(W, k + 1, n))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["staged", "pull"])
+def test_bench_gpus2_emulated_on_one_gpu(gpu_lib, transport):
+    """`bench.py --gpus 2` end to end on the one-GPU box: the launcher spawns
+    two ranks (gloo group, both on GPU 0), each uploads its half of B into a
+    CUDA-IPC-exported slice, gathers the other rank's half and computes its
+    row shard; the line must report two ranks and every rank's shard must
+    equal a one-shot GEMM of it bit for bit.  No cross-rank kernel waits:
+    the slices are resident before a barrier, then only read."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--emulate-on-one-gpu",
+           "--workload", "dd1024", "--extra", "qd1024", "--steps", "2", "--warmup", "1", "--no-cpu-baseline",
+           "--transport", transport]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["emulated_on_one_gpu"] is True
+    assert line["comm"] == {"backend": "gloo", "nranks": 2}
+    assert line["check_sharded_equals_one_shot"] is True
+    assert line["workloads"]["qd1024"]["check_sharded_equals_one_shot"] is True
+    assert len(line["per_rank_kernel_ms"]) == 2 and line["rows_per_rank"] == 512
+    assert line["peer_bytes_per_step"] == 8 * 2 * 512 * 1024
+    assert ("device_staged" if transport == "staged" else "device_pull") in line["transport"]
