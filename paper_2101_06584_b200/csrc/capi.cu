@@ -1203,8 +1203,9 @@ int mpfk_ew_apply_into(int width, int op, mpfk_mat* out, const mpfk_mat* a, cons
       grow(D.dB, D.capB, sizeof(double) * width * ps);
       grow(D.dC, D.capC, sizeof(double) * width * ps);
       const uint64_t pa = plane_of(a), pb = plane_of(b), po = plane_of(out);
-      const bool a_pin = host_operand_pinned(a->base, width, pa), b_pin = host_operand_pinned(b->base, width, pb),
-                 o_pin = host_operand_pinned(out->base, width, po);
+      const bool a_pin = host_operand_pinned(a->base, width, a->rows, a->cols, a->stride, pa),
+                 b_pin = host_operand_pinned(b->base, width, b->rows, b->cols, b->stride, pb),
+                 o_pin = host_operand_pinned(out->base, width, out->rows, out->cols, out->stride, po);
       D.stage.reset();
       ck(cudaEventRecord(D.ev[0], D.stream), "event");
       for (int w = 0; w < width; ++w) {

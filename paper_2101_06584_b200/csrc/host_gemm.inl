@@ -299,9 +299,9 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     const uint64_t pk = ((k + np - 1) / np + 15) / 16 * 16;  // even: 16-byte cp.async rows
     return {(int)((k + pk - 1) / pk), pk};
   };
-  const bool a_pin = host_operand_pinned(A->base, W, plane_of(A));
-  const bool b_pin = host_operand_pinned(B->base, W, plane_of(B));
-  const bool c_pin = host_operand_pinned(C->base, W, plane_of(C));
+  const bool a_pin = host_operand_pinned(A->base, W, A->rows, A->cols, A->stride, plane_of(A));
+  const bool b_pin = host_operand_pinned(B->base, W, B->rows, B->cols, B->stride, plane_of(B));
+  const bool c_pin = host_operand_pinned(C->base, W, C->rows, C->cols, C->stride, plane_of(C));
   // (pageable operands keep the chunked path: measured, staging A's narrow
   // K-panel columns through the copy threads costs more than the single
   // launch saves)

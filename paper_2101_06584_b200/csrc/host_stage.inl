@@ -121,12 +121,17 @@ HostRegCache& host_reg_cache() {
   return *c;
 }
 
-// an operand buffer of W planes (plane stride in doubles) is page-locked,
-// registering it through the cache when that is enabled
-bool host_operand_pinned(const void* base, int W, uint64_t plane_stride) {
+// an operand of W planes (rows x cols, row stride `stride`, plane stride
+// `plane_stride`, in doubles) is page-locked, registering it through the
+// cache when that is enabled -- exactly the bytes the operand spans, from
+// its first cell to the last cell of its last plane, never beyond
+bool host_operand_pinned(const void* base, int W, uint64_t rows, uint64_t cols, uint64_t stride,
+                         uint64_t plane_stride) {
   if (!base) return true;
   if (is_pinned(base)) return true;
-  return host_reg_cache().ensure(base, sizeof(double) * size_t(W) * plane_stride);
+  if (!rows || !cols) return false;
+  const uint64_t span = uint64_t(W - 1) * plane_stride + (rows - 1) * stride + cols;
+  return host_reg_cache().ensure(base, sizeof(double) * size_t(span));
 }
 
 // persistent workers running one job at a time: f(worker, workers)

@@ -181,9 +181,9 @@ void host_strassen(int W, mpfk_mat* Cm, const mpfk_mat* A, const mpfk_mat* B, ui
   grow(D.dB, D.capB, sizeof(double) * W * std::max<uint64_t>(K * ldb, 1));
   grow(D.dC, D.capC, sizeof(double) * W * std::max<uint64_t>(m * ldc, 1));
   const uint64_t pa = plane_of(A), pb = plane_of(B), pc = plane_of(Cm);
-  const bool a_pin = host_operand_pinned(A->base, W, plane_of(A)),
-             b_pin = host_operand_pinned(B->base, W, plane_of(B));
-  const bool c_pin = host_operand_pinned(Cm->base, W, plane_of(Cm));
+  const bool a_pin = host_operand_pinned(A->base, W, A->rows, A->cols, A->stride, plane_of(A)),
+             b_pin = host_operand_pinned(B->base, W, B->rows, B->cols, B->stride, plane_of(B));
+  const bool c_pin = host_operand_pinned(Cm->base, W, Cm->rows, Cm->cols, Cm->stride, plane_of(Cm));
   D.stage.reset();
   ck(cudaEventRecord(D.ev[0], D.stream), "event");
   for (int w = 0; w < W; ++w) {

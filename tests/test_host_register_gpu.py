@@ -24,7 +24,10 @@ def test_registered_operands_bit_identical(gpu_lib, W, n):
             assert P.bits_equal(C, want)
             P.host_unregister(C)
         st = P.host_register_cache_stats()
-        assert st["entries"] >= 2 and st["used"] >= 2 * 8 * W * n * P.pad_columns(n)
+        # A and B stay registered: each exactly its span, first cell to the
+        # last cell of its last plane
+        span = 8 * ((W * n - 1) * P.pad_columns(n) + n)
+        assert st["entries"] >= 2 and st["used"] >= 2 * span
     finally:
         P.host_register_cache(0)
     assert P.host_register_cache_stats()["entries"] == 0
@@ -33,7 +36,7 @@ def test_registered_operands_bit_identical(gpu_lib, W, n):
 def test_cache_is_bounded_lru(gpu_lib):
     P = gpu_lib
     W, n = 2, 512
-    bytes_one = 8 * W * n * P.pad_columns(n)
+    bytes_one = 8 * ((W * n - 1) * P.pad_columns(n) + n)  # the registered span of one operand
     mats = [P.fill_baseline(W, n, n, s) for s in range(4)]
     C = P.MPMatrix(W, n, n)
     P.host_register_cache(3 * bytes_one)
