@@ -99,7 +99,7 @@ __device__ __forceinline__ void cp_async16_full(unsigned smem_addr, const void* 
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
           int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0, int VSEBF_ = 0,
-          int FLOAD_ = 1>
+          int FLOAD_ = 1, int PAIRB_ = 1>
 struct TileCfg {
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
   static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
@@ -111,6 +111,10 @@ struct TileCfg {
   // interior tiles load full k-tiles with the precomputed-address loader
   // (FastLoad); 0 keeps the general loader everywhere
   static constexpr int FLOAD = FLOAD_;
+  // a thread's micro-tile columns in adjacent pairs (2 tx, 2 tx + 1, then
+  // + 2 TX ...) instead of stride TX, so each k step reads its B values with
+  // half as many (16-byte) shared loads; same bytes, same bank wavefronts
+  static constexpr int PAIRB = (PAIRB_ && TN_ % 2 == 0) ? 1 : 0;
   static constexpr int TX = BN / TN;  // threads along N
   static constexpr int TY = BM / TM;  // threads along M
   static constexpr int THREADS = TX * TY;
@@ -354,21 +358,47 @@ __device__ __noinline__ void wait_flag(const unsigned* f) {
   __syncthreads();
 }
 
+// column (within the tile) of micro-tile column j of thread column tx
+template <class Cfg>
+__device__ __forceinline__ int bcol(int tx, int j) {
+  if constexpr (Cfg::PAIRB) return 2 * tx + (j & 1) + (j >> 1) * (2 * Cfg::TX);
+  return tx + j * Cfg::TX;
+}
+
+// the thread's B values of k step kk from the stage
+template <class Cfg>
+__device__ __forceinline__ void load_b(double (&b)[Cfg::TN][Cfg::W], const double* Bs, int tx, int kk) {
+  constexpr int W = Cfg::W, BK = Cfg::BK, TN = Cfg::TN;
+  if constexpr (Cfg::PAIRB) {
+#pragma unroll
+    for (int jp = 0; jp < TN / 2; ++jp)
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const double2 v =
+            *reinterpret_cast<const double2*>(Bs + w * BK * Cfg::BS + kk * Cfg::BS + bcol<Cfg>(tx, 2 * jp));
+        b[2 * jp][w] = v.x;
+        b[2 * jp + 1][w] = v.y;
+      }
+  } else {
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+      for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + kk * Cfg::BS + bcol<Cfg>(tx, j)];
+  }
+}
+
 // one k step of the register micro-tile: C (+)= A(:, kk) * B(kk, :)
 template <class Cfg>
 __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W], const double* As,
                                          const double* Bs, int tx, int ty, int kk) {
-  constexpr int W = Cfg::W, BM = Cfg::BM, BK = Cfg::BK, TM = Cfg::TM, TN = Cfg::TN;
-  constexpr int TX = Cfg::TX, TY = Cfg::TY;
+  constexpr int W = Cfg::W, BM = Cfg::BM, TM = Cfg::TM, TN = Cfg::TN;
+  constexpr int TY = Cfg::TY;
   double a[TM][W], b[TN][W];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
-#pragma unroll
-  for (int j = 0; j < TN; ++j)
-#pragma unroll
-    for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + kk * Cfg::BS + tx + j * TX];
+  load_b<Cfg>(b, Bs, tx, kk);
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -384,17 +414,14 @@ __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W]
 template <class Cfg>
 __device__ __forceinline__ void mac_step_fast(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W], const double* As,
                                               const double* Bs, int tx, int ty, int kk, bool& rare) {
-  constexpr int W = Cfg::W, BM = Cfg::BM, BK = Cfg::BK, TM = Cfg::TM, TN = Cfg::TN;
-  constexpr int TX = Cfg::TX, TY = Cfg::TY;
+  constexpr int W = Cfg::W, BM = Cfg::BM, TM = Cfg::TM, TN = Cfg::TN;
+  constexpr int TY = Cfg::TY;
   double a[TM][W], b[TN][W];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
-#pragma unroll
-  for (int j = 0; j < TN; ++j)
-#pragma unroll
-    for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + kk * Cfg::BS + tx + j * TX];
+  load_b<Cfg>(b, Bs, tx, kk);
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -429,7 +456,7 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
-        const int gm = m0 + ty + i * TY, gn = n0 + tx + j * TX;
+        const int gm = m0 + ty + i * TY, gn = n0 + bcol<Cfg>(tx, j);
         const bool ok = gm < g.M && gn < g.N;
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[i][j][w] = ok ? g.C[w * g.pc + (long long)gm * g.ldc + gn] : 0.0;
@@ -509,10 +536,7 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS];
-#pragma unroll
-      for (int j = 0; j < TN; ++j)
-#pragma unroll
-        for (int w = 0; w < W; ++w) b[j][w] = Bs[w * BK * Cfg::BS + tx + j * TX];
+      load_b<Cfg>(b, Bs, tx, 0);
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -564,7 +588,7 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
     if (gm >= g.M) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int gn = n0 + tx + j * TX;
+      const int gn = n0 + bcol<Cfg>(tx, j);
       if (gn >= g.N) continue;
 #pragma unroll
       for (int w = 0; w < W; ++w) g.C[w * g.pc + (long long)gm * g.ldc + gn] = acc[i][j][w];

@@ -162,6 +162,23 @@ const Entry kEntries[] = {
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 1>>},
     {4, "fl0/4/32x32/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0>>,
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0>>},
+    // paired B columns (TileCfg::PAIRB) on / off, product configurations
+    {2, "pb1/2/64x64/product", run_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1>>,
+     info_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1>>},
+    {2, "pb0/2/64x64/product", run_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 0>>,
+     info_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 0>>},
+    {2, "pb1/2/32x32/product", run_cfg<TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1>>,
+     info_cfg<TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1>>},
+    {2, "pb0/2/32x32/product", run_cfg<TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 0>>,
+     info_cfg<TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 0>>},
+    {3, "pb1/3/32x32/product", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 1>>},
+    {3, "pb0/3/32x32/product", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 0>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 0>>},
+    {4, "pb1/4/32x32/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 1>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 1>>},
+    {4, "pb0/4/32x32/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>},
     // n = 1024 in ONE resident round: 1024 32x32 tiles on 148 SMs x 7 CTAs
     // of 128 threads (2x4 / 4x2 micro-tiles; BK 8 so 7 CTAs fit in smem)
     {2, "r2/2/32x32x8/2x4/ku8/mb7/fixk/onebar", run_cfg<TileCfg<2, 32, 32, 8, 2, 4, 2, 8, 16, 7, 1, 1>>,
