@@ -179,6 +179,24 @@ const Entry kEntries[] = {
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 1>>},
     {4, "pb0/4/32x32/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>,
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>},
+    // TD / QD n = 1024: finer tiles (2048 per launch) so the last resident
+    // round is a smaller share of the launch
+    {3, "fine/3/32x16/2x1/mb2", run_cfg<TileCfg<3, 32, 16, 16, 2, 1, 2, 1, 16, 2, 0, 0, 1, 1, 1, 0>>,
+     info_cfg<TileCfg<3, 32, 16, 16, 2, 1, 2, 1, 16, 2, 0, 0, 1, 1, 1, 0>>},
+    {3, "fine/3/32x16/2x1/mb3", run_cfg<TileCfg<3, 32, 16, 16, 2, 1, 2, 1, 16, 3, 0, 0, 1, 1, 1, 0>>,
+     info_cfg<TileCfg<3, 32, 16, 16, 2, 1, 2, 1, 16, 3, 0, 0, 1, 1, 1, 0>>},
+    {3, "fine/3/16x32/1x2/mb3", run_cfg<TileCfg<3, 16, 32, 16, 1, 2, 2, 1, 16, 3, 0, 0, 1, 1, 1, 0>>,
+     info_cfg<TileCfg<3, 16, 32, 16, 1, 2, 2, 1, 16, 3, 0, 0, 1, 1, 1, 0>>},
+    {3, "fine/3/32x32/2x2/product", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 0>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 0>>},
+    {4, "fine/4/32x16/2x1/mb2", run_cfg<TileCfg<4, 32, 16, 16, 2, 1, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>,
+     info_cfg<TileCfg<4, 32, 16, 16, 2, 1, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>},
+    {4, "fine/4/32x16/2x1/mb3", run_cfg<TileCfg<4, 32, 16, 16, 2, 1, 2, 4, 16, 3, 1, 1, 2, 0, 0, 0>>,
+     info_cfg<TileCfg<4, 32, 16, 16, 2, 1, 2, 4, 16, 3, 1, 1, 2, 0, 0, 0>>},
+    {4, "fine/4/16x32/1x2/mb3", run_cfg<TileCfg<4, 16, 32, 16, 1, 2, 2, 4, 16, 3, 1, 1, 2, 0, 0, 0>>,
+     info_cfg<TileCfg<4, 16, 32, 16, 1, 2, 2, 4, 16, 3, 1, 1, 2, 0, 0, 0>>},
+    {4, "fine/4/32x32/2x2/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>},
     // n = 1024 in ONE resident round: 1024 32x32 tiles on 148 SMs x 7 CTAs
     // of 128 threads (2x4 / 4x2 micro-tiles; BK 8 so 7 CTAs fit in smem)
     {2, "r2/2/32x32x8/2x4/ku8/mb7/fixk/onebar", run_cfg<TileCfg<2, 32, 32, 8, 2, 4, 2, 8, 16, 7, 1, 1>>,
