@@ -57,6 +57,21 @@ cudaError_t info_tma_cfg(int* regs, int* smem, int* threads) {
 }
 
 template <class Cfg>
+cudaError_t run_tma2_cfg(const GemmArgs& g, cudaStream_t s) {
+  return launch_tma2<Cfg>(g, s);
+}
+
+template <class Cfg>
+cudaError_t info_tma2_cfg(int* regs, int* smem, int* threads) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, mpgemm_tma2_kernel<Cfg>);
+  *regs = a.numRegs;
+  *smem = (int)TmaLayout2<Cfg>::SMEM;
+  *threads = Cfg::THREADS;
+  return e;
+}
+
+template <class Cfg>
 cudaError_t info_cfg(int* regs, int* smem, int* threads) {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, mpgemm_kernel<Cfg>);
@@ -179,6 +194,15 @@ const Entry kEntries[] = {
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 1>>},
     {4, "pb0/4/32x32/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>,
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>},
+    // TMA staging, dense tiles, no loader code in the FP64 warps (gemm_tma.cuh: tma2)
+    {2, "tma2/2/64x64/pb1/mb2", run_tma2_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1>>,
+     info_tma2_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1>>},
+    {2, "tma2/2/32x32/pb1/mb4", run_tma2_cfg<TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1>>,
+     info_tma2_cfg<TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1>>},
+    {2, "tma2/2/64x64/pb1/st3/mb2", run_tma2_cfg<TileCfg<2, 64, 64, 16, 4, 4, 3, 16, 16, 2, 1, 1, 0, 0, 1, 1>>,
+     info_tma2_cfg<TileCfg<2, 64, 64, 16, 4, 4, 3, 16, 16, 2, 1, 1, 0, 0, 1, 1>>},
+    {2, "pb1/2/64x64/product(again)", run_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1>>,
+     info_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1>>},
     // TD / QD n = 1024: finer tiles (2048 per launch) so the last resident
     // round is a smaller share of the launch
     {3, "fine/3/32x16/2x1/mb2", run_cfg<TileCfg<3, 32, 16, 16, 2, 1, 2, 1, 16, 2, 0, 0, 1, 1, 1, 0>>,
