@@ -309,6 +309,19 @@ def run_reference(args, n_gpus):
     line["cpu_baseline"]["warmup_sample"] = (f"the timed sample once, then {ref.warm_rows} rows (one wave) per "
                                              "further warm-up step")
     line["cpu_baseline"]["step_seconds_min_max"] = spread
+    # the other configs, each on a one-wave sample (one untimed call, then
+    # the median of two), next to the product arm's `workloads`
+    extras = {}
+    for w in extra_workloads(args):
+        r = CpuReference(w, waves=1)
+        r.step()
+        runs = [r.step() for _ in range(2)]
+        g = statistics.median(x for x, _ in runs)
+        extras[w] = {"value": round(g, 4), "ms_per_step": round(1e3 * statistics.median(t for _, t in runs), 2),
+                     "config": config_for(w, n_gpus), "cpu_baseline": r.describe(g)}
+        r.close()
+    if extras:
+        line["workloads"] = extras
     emit(line, args)
 
 

@@ -80,7 +80,7 @@ def test_bench_reference_arm_loads_no_product_library():
     """--impl reference runs the reference's CPU GEMM through oracle/ only:
     nothing of paper_2101_06584_b200 (or libmpfk.so) is imported or mapped."""
     code = ("import sys, json; sys.argv=['bench.py','--impl','reference','--steps','1','--warmup','1',"
-            "'--workload','dd1024','--cpu-waves','1']; import bench; bench.main(sys.argv[1:]); "
+            "'--workload','dd1024','--cpu-waves','1','--extra','td1024']; import bench; bench.main(sys.argv[1:]); "
             "maps=[l.split()[-1] for l in open('/proc/self/maps') if '.so' in l]; "
             "print(json.dumps({'mods':[m for m in sys.modules if m.startswith('paper_2101')], "
             "'libmpfk':[m for m in maps if 'libmpfk.so' in m], 'ref':[m for m in maps if 'libmpfkref' in m]}))")
@@ -90,4 +90,6 @@ def test_bench_reference_arm_loads_no_product_library():
     line, probe = out[0], out[-1]
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["config"] == __import__("bench").config_for("dd1024", 1)
+    assert line["workloads"]["td1024"]["value"] > 0  # the other configs, each with its own sample
+    assert line["workloads"]["td1024"]["config"] == __import__("bench").config_for("td1024", 1)
     assert probe["mods"] == [] and probe["libmpfk"] == [] and probe["ref"]
