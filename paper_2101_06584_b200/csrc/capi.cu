@@ -343,10 +343,11 @@ using Cfg2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1>;  // DD, fe
 // TD renorm5 paths A/B + td_mul's vseb common case (n=4096 0.978 -> 1.030 of
 // peak in counted ops), QD renorm5 path A only (0.928 -> 0.962).  Path B is
 // common for TD (its zero-extended fourth lane), so TD keeps it in the fast form.
-// Paired B columns (TileCfg::PAIRB, round 2; profiles/r02/tune_pairb.log): half
-// the B shared loads -- DD n=4096 +0.5 %, DD n=1024 +1 %; TD -0.3 % and QD
-// neutral, which keep the strided columns.
-using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 0>;  // TD: renorm5 A/B, vseb fast
+// Paired B columns (TileCfg::PAIRB, round 2; profiles/r02/tune_pairb.log,
+// tune_tdqd_flpb.log): half the B shared loads -- DD n=4096 +0.5 %, DD n=1024
+// +1 %, TD n=4096 +1.2 % with the 32-bit fast-loader state; QD neutral, it
+// keeps the strided columns and the general loader.
+using Cfg3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 1>;  // TD: renorm5 A/B, vseb fast
 // The interior fast loader (TileCfg::FLOAD, round 2; profiles/r02/tune_fload.log):
 // DD n=1024 1.330 -> 1.288 ms, DD n=4096 -0.7 %, TD n=4096 -0.5 %; QD keeps the
 // general loader (+0.5 % with it: its 128-register budget spills the loader state)

@@ -186,23 +186,28 @@ struct FastLoad {
 };
 
 struct FastLoadState {
-  const double* a;  // this thread's first A chunk at the current k-tile
-  const double* b;  // this thread's first B chunk at the current k-tile
-  unsigned sa, sb;  // their shared-memory offsets (bytes) within a stage
+  // this thread's first A / B chunk at the current k-tile, in elements from
+  // the plane base (32-bit: the fast loader runs only when a plane's
+  // offsets fit, fast_load_fits), and their shared-memory byte offsets
+  // within a stage -- four registers, so a 128-register kernel keeps them
+  unsigned a, b;
+  unsigned sa, sb;
 };
+
+__device__ __forceinline__ bool fast_load_fits(const GemmArgs& g) {
+  return (long long)g.M * g.lda < 0x7fffffffLL && ((long long)g.K + 64) * g.ldb < 0x7fffffffLL;
+}
 
 template <class Cfg>
 __device__ __forceinline__ FastLoadState fast_load_init(const GemmArgs& g, int m0, int n0, int k0) {
-  using F = FastLoad<Cfg>;
   const int tid = threadIdx.x;
   const int ra = tid / (Cfg::BK / 2), ka = 2 * (tid % (Cfg::BK / 2));
   const int rb = tid / (Cfg::BN / 2), nb = 2 * (tid % (Cfg::BN / 2));
   FastLoadState st;
-  st.a = g.A + (long long)(m0 + ra) * g.lda + k0 + ka;
-  st.b = g.B + (long long)(k0 + rb) * g.ldb + n0 + nb;
+  st.a = (unsigned)((m0 + ra) * (long long)g.lda + k0 + ka);
+  st.b = (unsigned)((k0 + rb) * (long long)g.ldb + n0 + nb);
   st.sa = 8u * (ra * Cfg::AS + ka);
   st.sb = 8u * (rb * Cfg::BS + nb);
-  (void)sizeof(F);
   return st;
 }
 
@@ -218,15 +223,15 @@ __device__ __forceinline__ void fast_load_tile(FastLoadState& st, double* As, do
 #pragma unroll
     for (int it = 0; it < F::A_IT; ++it)
       cp_async16_full(as + 8u * (w * Cfg::BM * Cfg::AS + it * F::A_ROWS * Cfg::AS),
-                      st.a + w * g.pa + (long long)(it * F::A_ROWS) * g.lda);
+                      g.A + w * g.pa + (long long)(it * F::A_ROWS) * g.lda + st.a);
 #pragma unroll
   for (int w = 0; w < W; ++w)
 #pragma unroll
     for (int it = 0; it < F::B_IT; ++it)
       cp_async16_full(bs + 8u * (w * Cfg::BK * Cfg::BS + it * F::B_ROWS * Cfg::BS),
-                      st.b + w * g.pb + (long long)(it * F::B_ROWS) * g.ldb);
+                      g.B + w * g.pb + (long long)(it * F::B_ROWS) * g.ldb + st.b);
   st.a += Cfg::BK;
-  st.b += (long long)Cfg::BK * g.ldb;
+  st.b += (unsigned)(Cfg::BK * g.ldb);
 }
 
 // linear CTA index -> (tile row, tile col) with GROUP_M-row bands
@@ -464,7 +469,7 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
   }
 
   // interior tile: every full k-tile takes the fast loader (FastLoad)
-  const bool interior = FastLoad<Cfg>::ok && m0 + BM <= g.M && n0 + Cfg::BN <= g.N;
+  const bool interior = FastLoad<Cfg>::ok && m0 + BM <= g.M && n0 + Cfg::BN <= g.N && fast_load_fits(g);
   const int kfull = g.K / BK;  // k-tiles [0, kfull) are full
   FastLoadState fl{};
   if (interior) fl = fast_load_init<Cfg>(g, m0, n0, 0);

@@ -194,6 +194,10 @@ const Entry kEntries[] = {
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 1>>},
     {4, "pb0/4/32x32/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>,
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>>},
+    {4, "fl1pb0/4/32x32", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 1, 0>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 1, 0>>},
+    {3, "fl0pb1/3/32x32", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 0, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 0, 1>>},
     // TMA staging, dense tiles, no loader code in the FP64 warps (gemm_tma.cuh: tma2)
     {2, "tma2/2/64x64/pb1/mb2", run_tma2_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1>>,
      info_tma2_cfg<TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1>>},
