@@ -80,6 +80,18 @@ inline OpCounts op_counters_read() {
   return c;
 }
 
+// Page-locking of long-lived pageable operands for the lifetime of a scope
+// (mpfk_host_register_cache): operands used inside are registered on first
+// use and all registrations are dropped when the scope ends -- so destroy
+// the matrices AFTER the scope, never inside it.
+class HostRegisterScope {
+ public:
+  explicit HostRegisterScope(std::uint64_t capacity_bytes) { mpfk_host_register_cache(capacity_bytes); }
+  ~HostRegisterScope() { mpfk_host_register_cache(0); }
+  HostRegisterScope(const HostRegisterScope&) = delete;
+  HostRegisterScope& operator=(const HostRegisterScope&) = delete;
+};
+
 namespace detail {
 
 // status -> the reference's exception types (config.hpp:25-28,

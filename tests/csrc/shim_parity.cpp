@@ -127,6 +127,20 @@ void drop_in(std::size_t m, std::size_t k, std::size_t n) {
   if constexpr (W == 3) {
     verdict(ref::bits_equal(ref::ew_add_merge(X, Y), la::ew_add_merge(X, Y)), tag + "ew_add_merge bits_equal");
   }
+  // the reference's own aligned_alloc'ed buffers page-locked for a scope
+  // (exact operand spans, mpfk_host_register_cache): same bits, registered
+  {
+    la::HostRegisterScope pin(std::uint64_t(1) << 30);
+    ref::MPMatrix<W> Cp(m, n);
+    la::matmul_block_parallel_into(Cp, A, B, 32, la::KernelVariant::SIMD_LOADSTORE, 1);
+    la::matmul_block_parallel_into(Cp, A, B, 32, la::KernelVariant::SIMD_LOADSTORE, 1);
+    std::uint64_t cap = 0, used = 0, ents = 0;
+    mpfk_host_register_cache_stats(&cap, &used, &ents);
+    const bool big = sizeof(double) * W * m * A.stride() >= (std::size_t(1) << 20);
+    verdict(ref::bits_equal(Cr, Cp) && (!big || ents >= 1),
+            tag + "page-locked reference buffers (" + std::to_string(ents) + " registered) bits_equal");
+    mpfk_host_unregister(Cp.plane(0));
+  }
   // MPFM round trip through the shim (the reference's linalg_io.cpp needs Boost)
   const std::string path = "/tmp/shim_parity_" + std::to_string(getpid()) + "_" + std::to_string(W) + ".mpfm";
   la::save_matrix_binary(Cr, path);
@@ -182,6 +196,7 @@ int main(int argc, char** argv) {
   expect_throw([&] { mpfk::linalg::matmul_block_parallel_into<2>(c, a, ok_b, 32, mpfk::linalg::KernelVariant::NORMAL, 0); },
                "matmul: workers must be at least 1");
   drop_in<2>(n, n + 3, n - 5);
+  drop_in<2>(600, 512, 600);  // operands >= 1 MiB: the registration cache engages
   drop_in<3>(70, 45, 50);
   drop_in<4>(33, 40, 36);
   drop_in_errors();
