@@ -1,7 +1,7 @@
 """Randomised parity sweep (one-off evidence, not a unit test): random widths,
 shapes, host-buffer kinds, device counts (MPFK_EMULATED_DEVICES), device
 entry points with offset windows, K-panel continuation, fused all-gather
-(pull and copy-engine variants) -- every result compared bit for bit with
+(pull, copy-engine flag-gated and staged variants) -- every result compared bit for bit with
 the reference build.  python scripts/fuzz_parity.py [cases] [seed] [host threads]"""
 import os
 import sys
@@ -140,10 +140,15 @@ def one_case(t, rng):
             P.gemm_device_pull(W, m, n, k, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), ld, k * ld,
                                dC.data_ptr(), ld, m * ld, ptrs, cuts, pr, int(rng.integers(1, 9)))
             what = f"pull cuts={cuts} panel={pr}"
-        else:
+        elif rng.integers(0, 2) == 0:
             P.gemm_device_gathered(W, m, n, k, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), ld,
                                    k * ld, dC.data_ptr(), ld, m * ld, ptrs, cuts, pr)
             what = f"gathered cuts={cuts} panel={pr}"
+        else:  # staged: copy-engine gather in growing K panels, one launch per panel
+            head = 16 * int(rng.integers(0, 5))
+            P.gemm_device_staged(W, m, n, k, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), ld,
+                                 k * ld, dC.data_ptr(), ld, m * ld, ptrs, cuts, head)
+            what = f"staged cuts={cuts} head={head}"
         torch.cuda.synchronize()
         got = dC.cpu().numpy()
     torch.cuda.synchronize()
