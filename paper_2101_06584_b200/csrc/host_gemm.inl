@@ -330,6 +330,25 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     fast_split[g] = fast && rows && splitk_plan(W, rows, n, K).S > 1;
     bounds[g] = fast_split[g] ? std::vector<uint64_t>{0, rows} : chunk_bounds(rows);
   }
+  // One GPU, page-locked A and B, K long enough for panels: chunk 0's A goes
+  // up in the same K panels as B (its narrow column blocks are plain DMA), so
+  // the first GEMM starts after one small panel instead of a whole A chunk;
+  // the panels grow 4x from 64 k rows, each panel's upload hiding under the
+  // previous panel's GEMM (chunk 0 = the first two standard chunks, so its
+  // compute per k row is ~5x the upload of a B row plus its A column).
+  const bool kpanel0 = G == 1 && a_pin && b_pin && !fast_split[0] && panels_of(K).first > 1 &&
+                       bounds[0].size() > 3;
+  if (kpanel0) bounds[0].erase(bounds[0].begin() + 1);
+  std::vector<uint64_t> cuts{0};
+  if (kpanel0) {
+    for (uint64_t h = 64; (int)cuts.size() < kMaxChunks && cuts.back() + h < K && h * 2 <= K - cuts.back(); h *= 4)
+      cuts.push_back(cuts.back() + h);
+    cuts.push_back(K);
+  } else {
+    const auto pp = panels_of(K);
+    for (int p = 1; p <= pp.first; ++p) cuts.push_back(std::min<uint64_t>(K, p * pp.second));
+  }
+  const int ncuts = (int)cuts.size() - 1;
   auto upload_a = [&](int g, int c) {  // A row chunk c of shard g
     Shard& s = sh[g];
     Device& D = g_dev[s.dev];
@@ -350,7 +369,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   const bool early0 = G == 1 && !b_pin && panels_of(K).first > 1 && panel_split0;
   auto gemm_chunk0_panel = [&](Device& D, int p) {
     const uint64_t rows = m, c1 = bounds[0][1];
-    const uint64_t pk = panels_of(K).second, k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
+    const uint64_t k0 = cuts[p], k1 = cuts[p + 1];
     if (p == 0) ck(cudaStreamWaitEvent(D.stream, D.evA[0], 0), "wait A chunk");
     ck(cudaStreamWaitEvent(D.stream, D.evB[p], 0), "wait B panel");
     return enqueue_gemm(W, c1, n, k1 - k0, D.dA + k0, lda, rows * lda, D.dB + k0 * ldb, ldb, K * ldb, D.dC, ldc,
@@ -367,12 +386,24 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     nchunks[g] = rows ? (int)bounds[g].size() - 1 : 0;
     ck(cudaEventRecord(D.ev[0], D.up), "event");
     if (early0) ck(cudaEventRecord(D.ev[2], D.stream), "event");
-    if (nchunks[g]) upload_a(g, 0);
-    const auto ppair = panels_of(s.b1 - s.b0);
-    const int np = ppair.first;
-    const uint64_t pk = ppair.second;
-    for (int p = 0; p < np; ++p) {
-      const uint64_t k0 = s.b0 + p * pk, k1 = std::min<uint64_t>(s.b1, k0 + pk);
+    if (nchunks[g] && !kpanel0) upload_a(g, 0);
+    // B's own rows in panels: the K cuts on one GPU, uniform panels of the
+    // GPU's 1/G slice otherwise
+    std::vector<uint64_t> bc;
+    if (G == 1) {
+      bc = cuts;
+    } else {
+      const auto ppair = panels_of(s.b1 - s.b0);
+      for (int p = 0; p <= ppair.first; ++p) bc.push_back(std::min<uint64_t>(s.b1, s.b0 + p * ppair.second));
+    }
+    for (int p = 0; p + 1 < (int)bc.size(); ++p) {
+      const uint64_t k0 = bc[p], k1 = bc[p + 1];
+      if (kpanel0 && nchunks[g]) {  // chunk 0's A columns [k0, k1) with the panel
+        const uint64_t c1 = bounds[g][1];
+        for (int w = 0; w < W; ++w)
+          copy_h2d(D, a_pin, D.dA + w * rows * lda + k0, lda, A->base + w * pa_h + s.r0 * A->stride + k0,
+                   A->stride, k1 - k0, c1, D.up);
+      }
       for (int w = 0; w < W; ++w)
         if (k1 > k0)
           copy_h2d(D, b_pin, D.dB + w * K * ldb + k0 * ldb, ldb, B->base + w * pb_h + k0 * B->stride, B->stride, n,
@@ -380,6 +411,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
       ck(cudaEventRecord(D.evB[p], D.up), "event");
       if (early0 && nchunks[g]) launches[g] += gemm_chunk0_panel(D, p);
     }
+    if (kpanel0 && nchunks[g]) ck(cudaEventRecord(D.evA[0], D.up), "event");
     ck(cudaEventRecord(D.ev[1], D.up), "event");
     if (!defer_a)
       for (int c = 1; c < nchunks[g]; ++c) upload_a(g, c);
@@ -415,14 +447,13 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
       ck(cudaEventRecord(D.ev[5], D.stream), "event");  // B complete on this GPU
     }
     const cudaEvent_t b_ready = peer ? D.ev[5] : D.ev[1];
-    const auto ppair = panels_of(K);
-    const int np = ppair.first;
-    const uint64_t pk = ppair.second;
+    const int np = ncuts;
     for (int c = 0; c < nchunks[g]; ++c) {
       cudaStream_t cs = (c & 1) ? D.stream2 : D.stream;
       const uint64_t c0 = bounds[g][c], c1 = bounds[g][c + 1];
       if (defer_a && c > 0) upload_a(g, c);
-      ck(cudaStreamWaitEvent(cs, D.evA[c], 0), "wait A chunk");
+      // (kpanel0: chunk 0's A arrives with the B panels; each panel's event covers both)
+      if (!(kpanel0 && c == 0)) ck(cudaStreamWaitEvent(cs, D.evA[c], 0), "wait A chunk");
       if (c == 0 && early0) {
         // enqueued panel by panel in phase1
       } else if (fast_split[g]) {  // one chunk: the whole shard
@@ -431,7 +462,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
                                          K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs);
       } else if (c == 0 && np > 1) {
         for (int p = 0; p < np; ++p) {
-          const uint64_t k0 = p * pk, k1 = std::min<uint64_t>(K, k0 + pk);
+          const uint64_t k0 = cuts[p], k1 = cuts[p + 1];
           ck(cudaStreamWaitEvent(cs, D.evB[p], 0), "wait B panel");
           launches[g] += enqueue_gemm(W, c1 - c0, n, k1 - k0, D.dA + c0 * lda + k0, lda, rows * lda,
                                       D.dB + k0 * ldb, ldb, K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs,
