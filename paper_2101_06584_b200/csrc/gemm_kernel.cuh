@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "mpf_arith.cuh"
 
 namespace mpfk {
@@ -99,7 +101,7 @@ __device__ __forceinline__ void cp_async16_full(unsigned smem_addr, const void* 
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
           int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0, int VSEBF_ = 0,
-          int FLOAD_ = 1, int PAIRB_ = 1>
+          int FLOAD_ = 1, int PAIRB_ = 1, int RAREMIN_ = 0>
 struct TileCfg {
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
   static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
@@ -125,6 +127,12 @@ struct TileCfg {
   // same order): bit-identical, and the common path has no branch
   static constexpr int FASTR = (W_ >= 3) ? FASTR_ : 0;  // renorm5_t level (1: paths A/B, 2: path A)
   static constexpr bool VSEBF = FASTR && VSEBF_;          // td_mul's vseb common case in the fast pass
+  // the fast pass's "left the fast form" accumulator: exact LOP3/PLOP3
+  // predicates (arith::RareBool, the product) or a running FMNMX3 minimum
+  // (arith::RareMin: 14 of TD's 48 and 83 of QD's 205 non-FP64 instructions
+  // per loop body fewer, yet 0.3-0.7 % SLOWER on the B200,
+  // profiles/r02/tune_raremin.log -- kept as a measured alternative)
+  using Rare = typename std::conditional<RAREMIN_ != 0, arith::RareMin, arith::RareBool>::type;
   static constexpr int SNAP = FASTR ? THREADS * TM * TN * W : 0;  // doubles
   static_assert(!FASTR || THREADS % 32 == 0, "the warp-level redo votes over full warps");
   static constexpr int APAD = 2, BPAD = 2;  // keep 16 B row alignment, spread banks
@@ -418,7 +426,8 @@ __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W]
 // `rare` when an input needed renorm5 paths C/D
 template <class Cfg>
 __device__ __forceinline__ void mac_step_fast(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W], const double* As,
-                                              const double* Bs, int tx, int ty, int kk, bool& rare) {
+                                              const double* Bs, int tx, int ty, int kk,
+                                              typename Cfg::Rare& rare) {
   constexpr int W = Cfg::W, BM = Cfg::BM, TM = Cfg::TM, TN = Cfg::TN;
   constexpr int TY = Cfg::TY;
   double a[TM][W], b[TN][W];
@@ -556,7 +565,7 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
         for (int j = 0; j < TN; ++j)
 #pragma unroll
           for (int w = 0; w < W; ++w) snap[((i * TN + j) * W + w) * Cfg::THREADS] = acc[i][j][w];
-      bool rare = false;
+      typename Cfg::Rare rare;
       if (Cfg::FIXK && kk == 0 && kend == BK) {
 #pragma unroll Cfg::KUNROLL
         for (int q = 0; q < BK; ++q) mac_step_fast<Cfg>(acc, As, Bs, tx, ty, q, rare);
@@ -564,7 +573,7 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
 #pragma unroll Cfg::KUNROLL
         for (int q = kk; q < kend; ++q) mac_step_fast<Cfg>(acc, As, Bs, tx, ty, q, rare);
       }
-      if (__any_sync(0xffffffffu, rare)) {  // rare: this warp redoes the k-tile exactly
+      if (__any_sync(0xffffffffu, rare.any())) {  // rare: this warp redoes the k-tile exactly
         if ((threadIdx.x & 31) == 0) atomicAdd(&g_fastr_redo, 1ull);
 #pragma unroll
         for (int i = 0; i < TM; ++i)

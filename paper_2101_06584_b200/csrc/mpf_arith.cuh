@@ -56,6 +56,54 @@ MPFK_HD bool nz(double x) {
 #endif
 MPFK_HD double sel(bool p, double a, double b) { return p ? a : b; }
 
+// "This input left the fast form" accumulators for the GEMM inner loop (the
+// `rare` argument of the *_t forms below): need_nz(x) records that x had to
+// be nonzero, any() reports whether some recorded x was zero.
+//
+// RareBool: the exact test (one LOP3 into a predicate per value plus the
+// predicate ORs).
+struct RareBool {
+  bool r = false;
+  MPFK_HD void need_nz(double x) { r |= !nz(x); }
+  MPFK_HD void need_nz(double x, double y) { r |= !(nz(x) & nz(y)); }
+  MPFK_HD void need_nz(double x, double y, double z) { r |= !(nz(x) & nz(y) & nz(z)); }
+  MPFK_HD bool any() const { return r; }
+};
+// RareMin: a running minimum of |high word read as binary32| -- one FMNMX3
+// with |.| operand modifiers per TWO values and nothing else, off the FP64
+// pipe.  x = +-0 has a high word of +-0.0f, so the minimum reaches 0.0f
+// whenever a recorded value was zero.  The test is conservative, never
+// optimistic: a subnormal below 2^-1042 (zero high word, nonzero low word)
+// also reads as zero, and the caller then merely recomputes with the exact
+// form.  High words that read as binary32 NaN (|x| >= 2^1017, infinities,
+// NaNs: nonzero) are skipped by fminf; binary32 subnormals (|x| < 2^-1015)
+// compare as what they are (no flush-to-zero in this build; a flush would
+// only be conservative).  MEASURED SLOWER than RareBool in the GEMMs
+// (profiles/r02/tune_raremin.log: TD n=4096 472.6 vs 469.4 ms, QD 852.0 vs
+// 848.2 ms) although the loop bodies shrink -- not the product's choice;
+// tests/test_arith_host.py checks the contract of both.
+struct RareMin {
+#if defined(__CUDA_ARCH__)
+  float m = 1.0f;
+  static MPFK_HD float key(double x) { return fabsf(__int_as_float(__double2hiint(x))); }
+  MPFK_HD void need_nz(double x) { m = fminf(m, key(x)); }
+  MPFK_HD void need_nz(double x, double y) { m = fminf(fminf(m, key(x)), key(y)); }
+  MPFK_HD void need_nz(double x, double y, double z) { need_nz(x, y), need_nz(z); }
+  MPFK_HD bool any() const { return m == 0.0f; }
+#else
+  bool r = false;
+  static MPFK_HD bool hz(double x) {
+    uint64_t u;
+    std::memcpy(&u, &x, sizeof u);
+    return (static_cast<uint32_t>(u >> 32) << 1) == 0;
+  }
+  MPFK_HD void need_nz(double x) { r |= hz(x); }
+  MPFK_HD void need_nz(double x, double y) { r |= hz(x) | hz(y); }
+  MPFK_HD void need_nz(double x, double y, double z) { r |= hz(x) | hz(y) | hz(z); }
+  MPFK_HD bool any() const { return r; }
+#endif
+};
+
 // ---------------------------------------------------------------------------
 // EFT primitives, eft.hpp:46-113.
 // ---------------------------------------------------------------------------
@@ -172,9 +220,9 @@ MPFK_HD void three_sum2(double a, double b, double c, double& s, double& e) {
 //      common (TD's zero-extended fourth lane makes it so).
 // Without the branch the compiler interleaves a thread's independent chains
 // across the renormalisation (TD/QD GEMM +2-3 %).
-template <int kFast, bool kTrunc3 = false>
+template <int kFast, bool kTrunc3 = false, class Rare = RareBool>
 MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, double& r0,
-                       double& r1, double& r2, double& r3, bool& rare) {
+                       double& r1, double& r2, double& r3, Rare& rare) {
   double t;
   qts(c3, c4, t, c4);
   qts(c2, t, t, c3);
@@ -184,14 +232,13 @@ MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, do
   double s0, s1, u, s2;
   qts(c0, c1, s0, s1);
   qts(s1, c2, u, s2);
-  const bool ab = nz(s1) & nz(s2);
-  if (kFast == 1) rare |= !ab;
+  if (kFast == 1) rare.need_nz(s1, s2);
   if (kFast == 2) {
     // path A only (all three forward residuals nonzero, eft.hpp:255-257):
     // no selects; path B (s3 == 0) and C/D count as rare
     double v, s3;
     qts(s2, c3, v, s3);
-    rare |= !(ab & nz(s3));
+    rare.need_nz(s1, s2, s3);
     r0 = s0;
     r1 = u;
     r2 = v;
@@ -209,7 +256,7 @@ MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, do
     r3 = 0.0;  // not an output (the caller truncates)
     return;
   }
-  if (kFast == 1 || ab) {
+  if (kFast == 1 || (nz(s1) & nz(s2))) {
     // path A (s3 != 0: s3 += c4) or path B (s3 == 0: s2 += c4), eft.hpp:255-260
     double v, s3;
     qts(s2, c3, v, s3);
@@ -256,7 +303,7 @@ MPFK_HD void renorm5_t(double c0, double c1, double c2, double c3, double c4, do
 
 MPFK_HD void renorm5(double c0, double c1, double c2, double c3, double c4, double& r0,
                      double& r1, double& r2, double& r3) {
-  bool rare = false;
+  RareBool rare;
   renorm5_t<0>(c0, c1, c2, c3, c4, r0, r1, r2, r3, rare);
 }
 
@@ -300,8 +347,8 @@ MPFK_HD void dd_mul(const double* x, const double* y, double* r) {
 // qd_add, mpf.hpp:178-196 (63 ops + renorm5).  With Trunc3 the fourth
 // output is not produced (td_add_q drops it, mpf.hpp:141), which lets the
 // compiler delete the dead tail of renorm5.
-template <bool Trunc3 = false, int kFast = 0>
-MPFK_HD void qd_add(const double* x, const double* y, double* r, bool& rare) {
+template <bool Trunc3 = false, int kFast = 0, class Rare = RareBool>
+MPFK_HD void qd_add(const double* x, const double* y, double* r, Rare& rare) {
   double s0, t0, s1, t1, s2, t2, s3, t3;
   two_sum(x[0], y[0], s0, t0);
   two_sum(x[1], y[1], s1, t1);
@@ -317,14 +364,14 @@ MPFK_HD void qd_add(const double* x, const double* y, double* r, bool& rare) {
 }
 template <bool Trunc3 = false>
 MPFK_HD void qd_add(const double* x, const double* y, double* r) {
-  bool rare = false;
+  RareBool rare;
   qd_add<Trunc3, 0>(x, y, r, rare);
 }
 
 // qd_mul, mpf.hpp:198-238 (111 ops + renorm5), including the pre-combined
 // operand pairs that keep it bitwise commutative (mpf.hpp:214-221).
-template <int kFast>
-MPFK_HD void qd_mul_t(const double* x, const double* y, double* r, bool& rare) {
+template <int kFast, class Rare = RareBool>
+MPFK_HD void qd_mul_t(const double* x, const double* y, double* r, Rare& rare) {
   double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
   two_prod(x[0], y[0], p0, q0);
   two_prod(x[0], y[1], p1, q1);
@@ -355,7 +402,7 @@ MPFK_HD void qd_mul_t(const double* x, const double* y, double* r, bool& rare) {
   renorm5_t<kFast>(p0, p1, s0, s1, s2, r[0], r[1], r[2], r[3], rare);
 }
 MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
-  bool rare = false;
+  RareBool rare;
   qd_mul_t<0>(x, y, r, rare);
 }
 
@@ -374,8 +421,8 @@ MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
 //  * t0 + t3 with t3 = +0 stays (same reason).
 // 11 of td_add_q's 85 FP64 operations disappear; results are unchanged
 // (tests/test_arith_host.py sweeps signed zeros against the reference).
-template <int kFast>
-MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, bool& rare) {
+template <int kFast, class Rare = RareBool>
+MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, Rare& rare) {
   double s0, t0, s1, t1, s2, t2;
   two_sum(x[0], y[0], s0, t0);
   two_sum(x[1], y[1], s1, t1);
@@ -392,7 +439,7 @@ MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, bool& rare)
   renorm5_t<kFast, true>(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3, rare);
 }
 MPFK_HD void td_add_q(const double* x, const double* y, double* r) {
-  bool rare = false;
+  RareBool rare;
   td_add_q_t<0>(x, y, r, rare);
 }
 
@@ -406,8 +453,8 @@ MPFK_HD void td_add_q_unfolded(const double* x, const double* y, double* r) {
 
 // td_mul, mpf.hpp:146-163 (41 ops + vseb).  kFast: vseb's common case only
 // (first residual nonzero: the two folds are the outputs), `rare` otherwise.
-template <bool kFast>
-MPFK_HD void td_mul_t(const double* x, const double* y, double* r, bool& rare) {
+template <bool kFast, class Rare = RareBool>
+MPFK_HD void td_mul_t(const double* x, const double* y, double* r, Rare& rare) {
   double z00s, z00e, z01s, z01e, z10s, z10e;
   two_prod(x[0], y[0], z00s, z00e);
   two_prod(x[0], y[1], z01s, z01e);
@@ -430,7 +477,7 @@ MPFK_HD void td_mul_t(const double* x, const double* y, double* r, bool& rare) {
   if (kFast) {
     double a, rr, b, r2;
     qts(e1, e2, a, rr);
-    rare |= !nz(rr);
+    rare.need_nz(rr);
     qts(rr, e3, b, r2);
     r[1] = a, r[2] = b;
   } else {
@@ -438,7 +485,7 @@ MPFK_HD void td_mul_t(const double* x, const double* y, double* r, bool& rare) {
   }
 }
 MPFK_HD void td_mul(const double* x, const double* y, double* r) {
-  bool rare = false;
+  RareBool rare;
   td_mul_t<false>(x, y, r, rare);
 }
 
@@ -589,15 +636,15 @@ MPFK_HD void mp_mul(const double* x, const double* y, double* r) {
 // 2 path A), kVseb = td_mul's vseb common case only; `rare` reports an input
 // that left the fast form (the result must then be recomputed exactly).  DD
 // has no data-dependent branch, so its fast form is the exact one.
-template <int W, int kRenorm>
-MPFK_HD void mp_add_f(const double* x, const double* y, double* r, bool& rare) {
+template <int W, int kRenorm, class Rare>
+MPFK_HD void mp_add_f(const double* x, const double* y, double* r, Rare& rare) {
   if constexpr (W == 2) dd_add(x, y, r);
   else if constexpr (W == 3) td_add_q_t<kRenorm>(x, y, r, rare);
   else qd_add<false, kRenorm>(x, y, r, rare);
 }
 
-template <int W, int kRenorm, bool kVseb>
-MPFK_HD void mp_mul_f(const double* x, const double* y, double* r, bool& rare) {
+template <int W, int kRenorm, bool kVseb, class Rare>
+MPFK_HD void mp_mul_f(const double* x, const double* y, double* r, Rare& rare) {
   if constexpr (W == 2) dd_mul(x, y, r);
   else if constexpr (W == 3) td_mul_t<kVseb>(x, y, r, rare);
   else qd_mul_t<kRenorm>(x, y, r, rare);

@@ -255,6 +255,24 @@ const Entry kEntries[] = {
      info_cfg<TileCfg<4, 64, 28, 16, 2, 2, 2, 4, 16, 1, 1, 1, 2>>},
     {4, "r2/4/32x32/2x2/ku4/mb2/fixk/onebar/fastr2(product)", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>>,
      info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2>>},
+    // the fast pass's departure accumulator (TileCfg::Rare): FMNMX3 running
+    // minimum (rm1) vs LOP3/PLOP3 predicates (rm0), product configurations
+    {3, "rm1/3/32x32/product", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 1, 1>>},
+    {3, "rm0/3/32x32/product", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 1, 0>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 1, 1, 1, 1, 0>>},
+    {4, "rm1/4/32x32/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0, 1>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0, 1>>},
+    {4, "rm0/4/32x32/product", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0, 0>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0, 0>>},
+    {4, "rm1/4/32x32/fl1", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 1, 0, 1>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 1, 0, 1>>},
+    {4, "rm1/4/32x32/pb1", run_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 1, 1>>,
+     info_cfg<TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 1, 1>>},
+    {3, "rm1/3/32x32/ku2", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 2, 16, 2, 0, 0, 1, 1, 1, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 2, 16, 2, 0, 0, 1, 1, 1, 1, 1>>},
+    {3, "rm1/3/32x32/onebar", run_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 1, 1, 1, 1, 1, 1>>,
+     info_cfg<TileCfg<3, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 1, 1, 1, 1, 1, 1>>},
 };
 
 // Compute-only ceiling of a tile configuration: the product's mac_step on

@@ -10,6 +10,29 @@
 
 using namespace mpfk::arith;
 
+// The GEMM fast pass's contract (gemm_kernel.cuh, TileCfg::FASTR): one
+// multiply-add acc = add(acc, mul(a, b)) in the fast forms (level 1 or 2,
+// vseb fast for TD) with both accumulators.  out per element: W doubles of
+// the fast result, then flags[2*i] = RareBool::any(), flags[2*i+1] =
+// RareMin::any().  The caller checks: fast == exact whenever the exact
+// accumulator stayed clear, and RareMin is never clear when RareBool is set.
+template <int W, int kLevel>
+static void fast_mac(const double* a, const double* b, const double* acc, double* out, int* flags) {
+  double p[W], r1[W], r2[W];
+  RareBool rb;
+  RareMin rm;
+  mp_mul_f<W, kLevel, true>(a, b, p, rb);
+  mp_add_f<W, kLevel>(acc, p, r1, rb);
+  mp_mul_f<W, kLevel, true>(a, b, p, rm);
+  mp_add_f<W, kLevel>(acc, p, r2, rm);
+  for (int w = 0; w < W; ++w) out[w] = r1[w];
+  flags[0] = rb.any();
+  flags[1] = rm.any();
+  // the accumulator type never changes the arithmetic
+  for (int w = 0; w < W; ++w)
+    if (std::memcmp(&r1[w], &r2[w], 8) != 0) flags[0] = flags[1] = -1;
+}
+
 extern "C" {
 
 int hst_binop_batch(int W, int op, std::size_t count, const double* x, const double* y,
@@ -87,6 +110,23 @@ void hst_two_sum_pair_batch(std::size_t count, const double* a, const double* b,
     two_sum_knuth(a[i], b[i], out[4 * i], out[4 * i + 1]);
     two_sum_sorted(a[i], b[i], out[4 * i + 2], out[4 * i + 3]);
   }
+}
+
+int hst_fast_mac_batch(int W, int level, std::size_t count, const double* a, const double* b,
+                       const double* acc, double* out, int* flags) {
+  for (std::size_t i = 0; i < count; ++i) {
+    const double *x = a + i * W, *y = b + i * W, *c = acc + i * W;
+    double* o = out + i * W;
+    int* f = flags + 2 * i;
+    switch (W * 4 + level) {
+      case 13: fast_mac<3, 1>(x, y, c, o, f); break;
+      case 14: fast_mac<3, 2>(x, y, c, o, f); break;
+      case 17: fast_mac<4, 1>(x, y, c, o, f); break;
+      case 18: fast_mac<4, 2>(x, y, c, o, f); break;
+      default: return 1;
+    }
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -231,3 +231,35 @@ def test_two_sum_sorted_equals_knuth(H):
     # and both orders of every pair
     H.hst_two_sum_pair_batch(n, b.ctypes.data, a.ctypes.data, out.ctypes.data)
     assert np.array_equal(out[:, :2].view(np.uint64), out[:, 2:].view(np.uint64))
+
+
+@pytest.mark.parametrize("W", [3, 4])
+@pytest.mark.parametrize("level", [1, 2])
+def test_fast_forms_flag_every_departure(H, W, level):
+    """The GEMM fast pass (TileCfg::FASTR): acc = add(acc, mul(a, b)) in the
+    branch-free forms equals the exact forms whenever the `rare` accumulator
+    stayed clear, for both accumulators; RareMin (FMNMX3 minimum of high
+    words) is conservative -- set whenever RareBool (exact zero tests) is."""
+    H.hst_fast_mac_batch.argtypes = [C.c_int, C.c_int, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p]
+    n = 60000
+    a = np.concatenate([_pairs(W, n // 2, 300 + W), _special_values(W, n // 2, 310 + W)])
+    b = np.concatenate([_pairs(W, n // 2, 320 + W), _special_values(W, n // 2, 330 + W)])
+    acc = np.concatenate([_pairs(W, n // 2, 340 + W), _special_values(W, n // 2, 350 + W)])
+    acc[::5] *= 2.0 ** -40
+    # exact cancellations of the leading terms and subnormal residues below
+    # 2^-1042 (zero high word, nonzero low word: RareMin reads them as zero)
+    p = O.ref_binop_batch(W, "mul", a, b)
+    acc[1::9] = -p[1::9]
+    acc[2::9, 1:] = 2.0 ** -1060
+    out = np.empty_like(a)
+    flags = np.zeros((n, 2), dtype=np.int32)
+    assert H.hst_fast_mac_batch(W, level, n, a.ctypes.data, b.ctypes.data, acc.ctypes.data, out.ctypes.data,
+                                flags.ctypes.data) == 0
+    assert (flags >= 0).all(), "the accumulator type changed the arithmetic"
+    want = O.ref_binop_batch(W, "add", acc, p)
+    clear = flags[:, 0] == 0
+    bad = (out.view(np.uint64) != want.view(np.uint64)).any(axis=1) & clear
+    assert not bad.any(), (a[bad][:3], b[bad][:3], acc[bad][:3])
+    assert not ((flags[:, 0] == 1) & (flags[:, 1] == 0)).any(), "RareMin missed a departure"
+    assert clear.sum() > 5000 and (~clear).sum() > 100  # both sides exercised
