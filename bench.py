@@ -84,6 +84,8 @@ def parse(argv=None):
     ap.add_argument("--cpu-waves", type=int, default=2,
                     help="CPU samples: waves of 32-row blocks per reference worker")
     ap.add_argument("--cpu-steps", type=int, default=3, help="cpu_baseline: timed reference calls (median)")
+    ap.add_argument("--no-lean", action="store_true",
+                    help="skip the MPFK_LEAN (tolerance mode) leg reported next to each bit-exact workload")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--transport", choices=TRANSPORTS, default=None,
                     help="N > 1 replication of B: staged (copy engines gather B's growing K panels from the "
@@ -531,6 +533,10 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
             del ref
         check = min(ctx.gather_float(1.0 if ok else 0.0)) == 1.0
 
+    lean = None
+    if ws == 1 and rows and not args.no_lean and transport not in ("nccl", "bcast"):
+        lean = measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream)
+
     step_ms = [a.elapsed_time(c) for a, _, c in evs]
     kern_ms = [b.elapsed_time(c) for _, b, c in evs]
     t_step_local = sum(step_ms) / len(step_ms)
@@ -609,6 +615,11 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
         "gpu_launches": n_launch,
         "clocks": clk,
     }
+    if lean is not None:
+        lean["frac_executed"] = round(rows * n * k * lean["ops_per_mac_executed"] /
+                                      (lean["ms_per_step"] * 1e-3) / 1e9 / peak, 4)
+        lean["speedup_vs_bit_exact"] = round(t_kern / lean["ms_per_step"], 3)
+        rec["lean"] = lean
     if e2e_pg is not None:
         rec["e2e_pageable"] = e2e_pg
     if cpu is not None:
@@ -635,6 +646,53 @@ def describe_transport(transport, ws, args, note):
         "bcast": "NCCL broadcast of B, then the GEMM",
     }[transport]
     return s + (f" [{note}]" if note else "")
+
+
+LEAN_OPS_PER_MAC = {2: 12 + 6 / 16, 3: 46 + 18 / 16, 4: 113 + 30 / 16}  # csrc/mpf_lean.cuh (+ renorm per 16-step k-tile)
+U_P = {2: 2.0 ** -104, 3: 2.0 ** -156, 4: 2.0 ** -208}  # north star
+
+
+def measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream):
+    """The same device-resident GEMM with flags = MPFK_LEAN (the north star's
+    tolerance mode: 12 / 46 / 113 FP64 instructions per multiply-add instead
+    of 20 / 119 / 218; NOT bit-identical to the reference).  Timed like the
+    bit-exact steps; its result is compared with theirs (dC, bit-identical to
+    the reference) as a normwise difference in units of 4*k*u_p."""
+    torch, P = ctx.torch, ctx.P
+    dL = torch.zeros_like(dC)
+
+    def step():
+        return P.gemm_device_ex(W, rows, n, k, dA.data_ptr(), ld, rows * ld, dB.data_ptr(), ld, k * ld,
+                                dL.data_ptr(), ld, rows * ld, P.LEAN, stream.cuda_stream)
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize(ctx.dev)
+    n_steps = max(2, min(steps, 5))
+    evs = []
+    for _ in range(n_steps):
+        if flush is not None:
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize(ctx.dev)
+    t = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+    # sum the component differences from the smallest up: the leading
+    # components cancel exactly where the two results agree
+    d = dL[W - 1] - dC[W - 1]
+    for w in range(W - 2, -1, -1):
+        d = d + (dL[w] - dC[w])
+    diff = float(d[:, :n].abs().max() / dC[0][:, :n].abs().max())
+    del dL, d
+    return {"flags": "MPFK_LEAN (tolerance mode; not bit-identical to the reference)",
+            "value": round(2.0 * rows * n * k / (t * 1e-3) / 1e9, 3), "unit": "Gflop/s",
+            "ms_per_step": round(t, 3), "steps": n_steps,
+            "ops_per_mac_executed": LEAN_OPS_PER_MAC[W],
+            "normwise_diff_vs_bit_exact": diff,
+            "tolerance_4ku_p": 4 * k * U_P[W],
+            "diff_over_tolerance": round(diff / (4 * k * U_P[W]), 6)}
 
 
 def measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned, dC_host, register=False):
@@ -726,7 +784,8 @@ def run_mpfk(args, ws, rank, local):
             "gpu_launches": head["gpu_launches"],
             "clocks": head["clocks"],
         }
-        for key in ("e2e_pageable", "per_rank_kernel_ms", "peer_bytes_per_step", "check_sharded_equals_one_shot"):
+        for key in ("lean", "e2e_pageable", "per_rank_kernel_ms", "peer_bytes_per_step",
+                    "check_sharded_equals_one_shot"):
             if key in head:
                 line[key] = head[key]
         if ctx.comm is not None:

@@ -142,8 +142,21 @@ int mpfk_last_stats(mpfk_stats *out);
  *   reference-order chain, and the S partial products are added in a fixed
  *   order (mpf::add<W>); otherwise identical to MPFK_BIT_EXACT.
  *   Deterministic for a given shape and device; normwise relative error
- *   within 4*k*u_p (u_p = 2^-104 / 2^-156 / 2^-208). */
-enum mpfk_flags { MPFK_BIT_EXACT = 0u, MPFK_FAST = 1u };
+ *   within 4*k*u_p (u_p = 2^-104 / 2^-156 / 2^-208).
+ * MPFK_LEAN: the north star's tolerance mode for the arithmetic itself.  The
+ *   reference renormalises to a canonical value after every multiply and
+ *   every add (mpf.hpp:105-238: 20 / 132 / 218 FP64 operations per
+ *   multiply-add); a GEMM element is one long sum, so this mode keeps each
+ *   element as W overlapping levels fed by exact two-sum cascades, pulls them
+ *   back once per 16 k steps and normalises once at the end
+ *   (csrc/mpf_lean.cuh: 12 / 46 / 113 FP64 instructions per multiply-add, 1.5x /
+ *   2.5x / 1.9x the bit-exact GEMM's rate on a B200).  NOT bit-identical to
+ *   the reference; results are canonical normalised values within the same
+ *   normwise 4*k*u_p (measured: 1e-4..4e-3 of it on the BASELINE inputs,
+ *   i.e. less accurate than the reference's own 4e-6..2e-4), deterministic
+ *   and independent of tiling, sharding and K panels.  May be combined with
+ *   MPFK_FAST (K segments keep the reference's arithmetic). */
+enum mpfk_flags { MPFK_BIT_EXACT = 0u, MPFK_FAST = 1u, MPFK_LEAN = 2u };
 
 /* The SURVEY's proposed entry point: C = A*B for host matrices in the
  * reference layout on n_gpus GPUs (<= 0: all visible), rows of C sharded

@@ -20,7 +20,7 @@
 //   ew_apply_into, ew_add, ew_mul, ew_add_merge   linalg.hpp:623-707
 //   save_matrix_binary / load_matrix_binary   linalg.hpp:716-721 (linalg_io.cpp:66-111)
 //   op_counters_reset / op_counters_read      linalg.hpp:160-170 (linalg.cpp:10-25)
-//   gemm_into (flags BIT_EXACT / FAST)
+//   gemm_into (flags BIT_EXACT / FAST / LEAN) SURVEY.md 8(b)
 //
 // Op counts: every call bumps libmpfk's counters (mpfk::linalg::
 // op_counters_read) with the reference's semantics (count_matmul
@@ -181,7 +181,11 @@ void matmul_naive_into(Mat& C, const Mat& A, const Mat& B, V variant = V::NORMAL
 // mpfk_gemm: the SURVEY's proposed entry point with flags.  BIT_EXACT is
 // matmul_block_parallel_into on n_gpus GPUs (<= 0: all); FAST may split K
 // when the output cannot fill the GPU (deterministic, within 4*k*u_p).
-enum class GemmFlags : unsigned { BIT_EXACT = MPFK_BIT_EXACT, FAST = MPFK_FAST };
+enum class GemmFlags : unsigned {
+  BIT_EXACT = MPFK_BIT_EXACT,
+  FAST = MPFK_FAST,
+  LEAN = MPFK_LEAN,  // tolerance-mode arithmetic (mpfk.h); combine as GemmFlags(MPFK_FAST | MPFK_LEAN)
+};
 
 template <int W, class Mat>
 void gemm_into(Mat& C, const Mat& A, const Mat& B, int n_gpus = 1, GemmFlags flags = GemmFlags::BIT_EXACT) {

@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmpfk.so")
 
 MPFK_OK, MPFK_EINVAL, MPFK_ERUNTIME, MPFK_ECUDA, MPFK_ENOMEM, MPFK_ENODEV = range(6)
-MPFK_BIT_EXACT, MPFK_FAST = 0, 1  # mpfk_flags
+MPFK_BIT_EXACT, MPFK_FAST, MPFK_LEAN = 0, 1, 2  # mpfk_flags
 
 
 class MpfkMat(C.Structure):

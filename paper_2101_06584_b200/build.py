@@ -63,7 +63,7 @@ def build_host_arith(force=False):
     os.makedirs(outdir, exist_ok=True)
     out = os.path.join(outdir, "libarith_host.so")
     src = os.path.join(ROOT, "tests", "csrc", "arith_host.cpp")
-    if force or _stale(out, [src, os.path.join(CSRC, "mpf_arith.cuh")]):
+    if force or _stale(out, [src, os.path.join(CSRC, "mpf_arith.cuh"), os.path.join(CSRC, "mpf_lean.cuh")]):
         _run(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
               "-I", CSRC, "-o", out, src])
     return out

@@ -357,6 +357,15 @@ using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>; 
 // n=4096 (e2e 891 vs 864 ms; the per-panel flag wait after the k-tile's
 // barrier is the culprit -- 4-step tiles with two barriers measure 867 ms)
 using Cfg4g = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 2, 0, 0, 0>;
+// MPFK_LEAN (csrc/mpf_lean.cuh: 12 / 46 / 113 FP64 instructions per
+// multiply-add, tolerance mode).  Tiles from the sweep of csrc/tune_lean.cu
+// (scripts/tune.py --lean, profiles/r02/tune_lean.log): straight-line
+// k-tiles, one barrier, fast loader and paired B columns for every width;
+// TD at 3 CTAs/SM (80 registers), QD at 2.
+using CfgL2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1, 0, 1>;
+using CfgL2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1, 0, 1>;
+using CfgL3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 16, 16, 3, 1, 1, 0, 0, 1, 1, 0, 1>;
+using CfgL4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 0, 0, 1, 1, 0, 1>;
 
 template <class Cfg>
 void configure_once() {
@@ -401,6 +410,10 @@ double predicted_eff(const kern::GemmArgs& g, double steady) {
 bool dd_small_tiles(const kern::GemmArgs& g) {
   return predicted_eff<Cfg2s>(g, 0.935) > predicted_eff<Cfg2>(g, 0.948);
 }
+// the same rule for the lean DD tiles (steady: 0.859 / 0.870 of the pipe at n=4096)
+bool dd_small_tiles_lean(const kern::GemmArgs& g) {
+  return predicted_eff<CfgL2s>(g, 0.859) > predicted_eff<CfgL2>(g, 0.870);
+}
 
 template <class Cfg>
 void launch_cfg(const kern::GemmArgs& g, cudaStream_t s) {
@@ -422,13 +435,14 @@ __global__ void zero_planes_kernel(double* C, long long ldc, long long pc, int M
 }
 
 // Enqueue C = A*B on the current device.  Returns kernel launches.
-int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s);
+// lean: the MPFK_LEAN arithmetic (tolerance mode) instead of the reference's.
+int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s, bool lean = false);
 
 // accumulate: continue the chains already in C over this K panel (see
 // GemmArgs::accumulate); k == 0 is then a no-op.
 int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
                  uint64_t pa, const double* B, uint64_t ldb, uint64_t pb, double* C,
-                 uint64_t ldc, uint64_t pc, cudaStream_t s, bool accumulate = false) {
+                 uint64_t ldc, uint64_t pc, cudaStream_t s, bool accumulate = false, bool lean = false) {
   if (m == 0 || n == 0) return 0;
   if (k == 0 && accumulate) return 0;
   if (m > 0x7fffffffULL || n > 0x7fffffffULL || k > 0x7fffffffULL)
@@ -446,7 +460,7 @@ int enqueue_gemm(int W, uint64_t m, uint64_t n, uint64_t k, const double* A, uin
   g.M = (int)m, g.N = (int)n, g.K = (int)k;
   g.accumulate = accumulate ? 1 : 0;
   g.batch = 1, g.sa = g.sb = g.sc = 0;
-  return dispatch_gemm(W, g, s);
+  return dispatch_gemm(W, g, s, lean);
 }
 
 // A strided batch of `batch` products of one shape (Strassen leaves).
@@ -614,7 +628,21 @@ std::pair<int, int> dispatch_gemm_gated(int W, const kern::GemmArgs& g, const ke
   }
 }
 
-int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s) {
+int dispatch_gemm(int W, const kern::GemmArgs& g, cudaStream_t s, bool lean) {
+  if (lean) {
+    switch (W) {
+      case 2:
+        if (dd_small_tiles_lean(g))
+          launch_cfg<CfgL2s>(g, s);
+        else
+          launch_cfg<CfgL2>(g, s);
+        break;
+      case 3: launch_cfg<CfgL3>(g, s); break;
+      case 4: launch_cfg<CfgL4>(g, s); break;
+      default: fail(MPFK_EINVAL, "mpfk: width must be 2, 3 or 4");
+    }
+    return 1;
+  }
   switch (W) {
     case 2:
       if (dd_small_tiles(g))
@@ -1138,9 +1166,10 @@ int mpfk_gemm(int width, const mpfk_mat* A, const mpfk_mat* B, mpfk_mat* C, int 
     check_mat(B, "B");
     check_mat(C, "C");
     check_mul_shapes(A, B, C);
-    if (flags & ~unsigned(MPFK_FAST)) fail(MPFK_EINVAL, "mpfk: unknown flags");
+    if (flags & ~unsigned(MPFK_FAST | MPFK_LEAN)) fail(MPFK_EINVAL, "mpfk: unknown flags");
     // n_gpus <= 0: every visible device (host_gemm caps the count)
-    host_gemm(width, C, A, B, n_gpus > 0 ? (unsigned)n_gpus : 1u << 20, (flags & MPFK_FAST) != 0);
+    host_gemm(width, C, A, B, n_gpus > 0 ? (unsigned)n_gpus : 1u << 20, (flags & MPFK_FAST) != 0,
+              (flags & MPFK_LEAN) != 0);
   });
 }
 
@@ -1149,7 +1178,7 @@ int mpfk_gemm_device_ex(int width, uint64_t m, uint64_t n, uint64_t k, const dou
                         uint64_t ldc, uint64_t c_plane, unsigned flags, void* stream, int* launches) {
   return guarded([&] {
     check_width(width);
-    if (flags & ~unsigned(MPFK_FAST)) fail(MPFK_EINVAL, "mpfk: unknown flags");
+    if (flags & ~unsigned(MPFK_FAST | MPFK_LEAN)) fail(MPFK_EINVAL, "mpfk: unknown flags");
     if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
     if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
       fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
@@ -1159,10 +1188,12 @@ int mpfk_gemm_device_ex(int width, uint64_t m, uint64_t n, uint64_t k, const dou
     const int dev = current_device();
     ensure_devices(1, dev);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int l = (flags & MPFK_FAST) ? enqueue_gemm_fast(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc,
-                                                          c_plane, s)
-                                      : enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc,
-                                                     c_plane, s);
+    // MPFK_FAST splits K (segments in the reference's arithmetic) where the
+    // output cannot fill the GPU; otherwise MPFK_LEAN picks the arithmetic
+    const bool split = (flags & MPFK_FAST) && splitk_plan(width, m, n, k).S > 1;
+    const int l = split ? enqueue_gemm_fast(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, s)
+                        : enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, s,
+                                       false, (flags & MPFK_LEAN) != 0);
     count_matmul(m, n, k);
     if (launches) *launches = l;
   });

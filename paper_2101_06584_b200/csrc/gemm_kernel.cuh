@@ -31,6 +31,7 @@
 #include <type_traits>
 
 #include "mpf_arith.cuh"
+#include "mpf_lean.cuh"
 
 namespace mpfk {
 namespace kern {
@@ -101,8 +102,15 @@ __device__ __forceinline__ void cp_async16_full(unsigned smem_addr, const void* 
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
           int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0, int VSEBF_ = 0,
-          int FLOAD_ = 1, int PAIRB_ = 1, int RAREMIN_ = 0>
+          int FLOAD_ = 1, int PAIRB_ = 1, int RAREMIN_ = 0, int LEAN_ = 0>
 struct TileCfg {
+  // MPFK_LEAN (mpf_lean.cuh): the tolerance-mode multiply-accumulate --
+  // every element is W levels fed by exact two-sum cascades, pulled back to
+  // nearly non-overlapping once per k-tile and normalised once at the end.
+  // 12 / 46 / 113 FP64 instructions per step; NOT bit-identical to the
+  // reference (within the north star's 4*k*u_p).  No data-dependent path, so
+  // no FASTR machinery.
+  static constexpr int LEAN = LEAN_;
   static constexpr int W = W_, BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
   static constexpr int STAGES = STAGES_, KUNROLL = KUNROLL_, GROUP_M = GROUP_M_, MINB = MINB_;
   static constexpr int FIXK = FIXK_;  // full k-tiles run a constant-trip loop
@@ -125,7 +133,7 @@ struct TileCfg {
   // restores its chains from a shared-memory snapshot taken at the k-tile
   // start and recomputes the k-tile with the exact form (same smem stage,
   // same order): bit-identical, and the common path has no branch
-  static constexpr int FASTR = (W_ >= 3) ? FASTR_ : 0;  // renorm5_t level (1: paths A/B, 2: path A)
+  static constexpr int FASTR = (W_ >= 3 && !LEAN_) ? FASTR_ : 0;  // renorm5_t level (1: paths A/B, 2: path A)
   static constexpr bool VSEBF = FASTR && VSEBF_;          // td_mul's vseb common case in the fast pass
   // the fast pass's "left the fast form" accumulator: exact LOP3/PLOP3
   // predicates (arith::RareBool, the product) or a running FMNMX3 minimum
@@ -446,6 +454,24 @@ __device__ __forceinline__ void mac_step_fast(double (&acc)[Cfg::TM][Cfg::TN][Cf
     }
 }
 
+// one k step in the lean form (Cfg::LEAN): acc holds levels, not a value
+template <class Cfg>
+__device__ __forceinline__ void mac_step_lean(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W], const double* As,
+                                              const double* Bs, int tx, int ty, int kk) {
+  constexpr int W = Cfg::W, BM = Cfg::BM, TM = Cfg::TM, TN = Cfg::TN;
+  constexpr int TY = Cfg::TY;
+  double a[TM][W], b[TN][W];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
+  load_b<Cfg>(b, Bs, tx, kk);
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) arith::lean_mac<W>(acc[i][j], a[i], b[j]);
+}
+
 // One output tile (rows m0.., columns n0..) over the K range of g: the
 // k = 0 step initialises the chains unless g.accumulate, which continues the
 // chains stored in C.
@@ -465,6 +491,14 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
   const int ktiles = (g.K + BK - 1) / BK;
 
   double acc[TM][TN][W];
+  if (Cfg::LEAN && !g.accumulate) {  // the levels start at +0: no peeled first step
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[i][j][w] = 0.0;
+  }
   if (g.accumulate) {
 #pragma unroll
     for (int i = 0; i < TM; ++i)
@@ -543,7 +577,7 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
     const double* Bs = Bs0 + slot * Cfg::B_STAGE;
     const int kend = min(BK, g.K - kt * BK);
     int kk = 0;
-    if (kt == 0 && !g.accumulate) {
+    if (!Cfg::LEAN && kt == 0 && !g.accumulate) {
       // k == 0: the product initialises the element (linalg.hpp:242, 260-261)
       double a[TM][W], b[TN][W];
 #pragma unroll
@@ -557,7 +591,20 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
         for (int j = 0; j < TN; ++j) arith::mp_mul<W>(a[i], b[j], acc[i][j]);
       kk = 1;
     }
-    if constexpr (Cfg::FASTR) {
+    if constexpr (Cfg::LEAN) {
+      if (Cfg::FIXK && kend == BK) {
+#pragma unroll Cfg::KUNROLL
+        for (int q = 0; q < BK; ++q) mac_step_lean<Cfg>(acc, As, Bs, tx, ty, q);
+      } else {
+#pragma unroll Cfg::KUNROLL
+        for (int q = 0; q < kend; ++q) mac_step_lean<Cfg>(acc, As, Bs, tx, ty, q);
+      }
+      // once per k-tile: the levels back to nearly non-overlapping
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) arith::lean_renorm_loose<W>(acc[i][j]);
+    } else if constexpr (Cfg::FASTR) {
       double* snap = smem + STAGES * (Cfg::A_STAGE + Cfg::B_STAGE) + threadIdx.x;
 #pragma unroll
       for (int i = 0; i < TM; ++i)
@@ -596,6 +643,12 @@ __device__ __forceinline__ void tile_run(const GemmArgs& g, int m0, int n0, cons
   if (Cfg::ONEBAR) __syncthreads();  // the slots are free again (a persistent caller may refill them)
 
   if (ktiles == 0) return;  // K == 0 is handled by the host (C = +0)
+  if constexpr (Cfg::LEAN) {  // levels -> canonical normalised values
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) arith::lean_finish<W>(acc[i][j], acc[i][j]);
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int gm = m0 + ty + i * TY;

@@ -171,7 +171,11 @@ struct Shard {
 // ld = pad4(cols) (16-byte rows for cp.async), A shard rows only, full B.
 // fast: MPFK_FAST -- shards whose output cannot fill the GPU take the
 // split-K path (enqueue_gemm_fast); everything else is bit-exact.
-void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigned gpus, bool fast = false) {
+// lean: MPFK_LEAN -- every launch that is not a split-K one runs the lean
+// arithmetic (csrc/mpf_lean.cuh, tolerance mode); the chunked pipeline below
+// (the copy-engine-gated single launch has no lean instantiation).
+void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigned gpus, bool fast = false,
+               bool lean = false) {
   std::lock_guard<std::mutex> call_lock(g_call_mu);
   const auto t0 = std::chrono::steady_clock::now();
   const uint64_t m = A->rows, K = A->cols, n = B->cols;
@@ -305,7 +309,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
   // (pageable operands keep the chunked path: measured, staging A's narrow
   // K-panel columns through the copy threads costs more than the single
   // launch saves)
-  if (G == 1 && a_pin && b_pin && c_pin && K > 0 && !std::getenv("MPFK_CHUNKED_HOST") &&
+  if (G == 1 && a_pin && b_pin && c_pin && K > 0 && !lean && !std::getenv("MPFK_CHUNKED_HOST") &&
       gate_pays(W, m, n, K, 50e9) && memops_available() && !(fast && splitk_plan(W, m, n, K).S > 1)) {
     int prev = 0;
     cudaGetDevice(&prev);
@@ -373,7 +377,7 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
     if (p == 0) ck(cudaStreamWaitEvent(D.stream, D.evA[0], 0), "wait A chunk");
     ck(cudaStreamWaitEvent(D.stream, D.evB[p], 0), "wait B panel");
     return enqueue_gemm(W, c1, n, k1 - k0, D.dA + k0, lda, rows * lda, D.dB + k0 * ldb, ldb, K * ldb, D.dC, ldc,
-                        rows * ldc, D.stream, p > 0);
+                        rows * ldc, D.stream, p > 0, lean);
   };
   auto phase1 = [&](int g) {  // allocate; upload A chunk 0, B (slice or K panels), other A chunks
     Shard& s = sh[g];
@@ -466,12 +470,12 @@ void host_gemm(int W, mpfk_mat* C, const mpfk_mat* A, const mpfk_mat* B, unsigne
           ck(cudaStreamWaitEvent(cs, D.evB[p], 0), "wait B panel");
           launches[g] += enqueue_gemm(W, c1 - c0, n, k1 - k0, D.dA + c0 * lda + k0, lda, rows * lda,
                                       D.dB + k0 * ldb, ldb, K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs,
-                                      p > 0);
+                                      p > 0, lean);
         }
       } else {
         ck(cudaStreamWaitEvent(cs, b_ready, 0), "wait B");
         launches[g] += enqueue_gemm(W, c1 - c0, n, K, D.dA + c0 * lda, lda, rows * lda, D.dB, ldb,
-                                    K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs);
+                                    K * ldb, D.dC + c0 * ldc, ldc, rows * ldc, cs, false, lean);
       }
       ck(cudaEventRecord(D.evC[c], cs), "event");
       // pageable C: a staged download occupies this thread until its chunk

@@ -190,7 +190,7 @@ def matmul_naive_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix,
     N.check(N.lib().mpfk_matmul_naive_into(W, C.byref(c), C.byref(a), C.byref(b), int(variant)))
 
 
-BIT_EXACT, FAST = N.MPFK_BIT_EXACT, N.MPFK_FAST
+BIT_EXACT, FAST, LEAN = N.MPFK_BIT_EXACT, N.MPFK_FAST, N.MPFK_LEAN
 
 
 def gemm_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix, n_gpus: int = 1, flags: int = BIT_EXACT):

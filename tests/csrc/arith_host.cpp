@@ -5,8 +5,10 @@
 // without a GPU.  The device build uses __dadd_rn & co. with identical IEEE
 // semantics.
 #include <cstddef>
+#include <vector>
 
 #include "mpf_arith.cuh"
+#include "mpf_lean.cuh"
 
 using namespace mpfk::arith;
 
@@ -33,7 +35,107 @@ static void fast_mac(const double* a, const double* b, const double* acc, double
     if (std::memcmp(&r1[w], &r2[w], 8) != 0) flags[0] = flags[1] = -1;
 }
 
+// MPFK_LEAN (csrc/mpf_lean.cuh): the GEMM element's chain on the host --
+// levels start at +0 (or at a normalised `init`), every k step is one
+// lean_mac, renorm_loose every `every` steps (the kernel: once per 16-step
+// k-tile), lean_finish at the end.
+template <int W>
+static void lean_dot(std::size_t k, const double* a, const double* b, std::size_t every, const double* init,
+                     double* out) {
+  double s[W];
+  for (int w = 0; w < W; ++w) s[w] = init ? init[w] : 0.0;
+  for (std::size_t i = 0; i < k; ++i) {
+    lean_mac<W>(s, a + i * W, b + i * W);
+    // the kernel renormalises at the end of every k-tile, the last (partial) one included
+    if (every && ((i + 1) % every == 0 || i + 1 == k)) lean_renorm_loose<W>(s);
+  }
+  lean_finish<W>(s, out);
+}
+
+// the reference-order chain (mul, then add ascending k) with the product's
+// bit-exact arithmetic, for the error comparison
+template <int W>
+static void ref_dot(std::size_t k, const double* a, const double* b, double* out) {
+  double acc[W], p[W];
+  for (std::size_t i = 0; i < k; ++i) {
+    mp_mul<W>(a + i * W, b + i * W, p);
+    if (i == 0)
+      for (int w = 0; w < W; ++w) acc[w] = p[w];
+    else
+      mp_add<W>(acc, p, acc);
+  }
+  for (int w = 0; w < W; ++w) out[w] = k ? acc[w] : 0.0;
+}
+
 extern "C" {
+
+// count dot products of length k: a, b are (count, k, W); out (count, W)
+int hst_lean_dot_batch(int W, std::size_t count, std::size_t k, const double* a, const double* b,
+                       std::size_t every, const double* init, double* out) {
+  for (std::size_t c = 0; c < count; ++c) {
+    const double *x = a + c * k * W, *y = b + c * k * W;
+    const double* in = init ? init + c * W : nullptr;
+    double* o = out + c * W;
+    if (W == 2) lean_dot<2>(k, x, y, every, in, o);
+    else if (W == 3) lean_dot<3>(k, x, y, every, in, o);
+    else if (W == 4) lean_dot<4>(k, x, y, every, in, o);
+    else return 1;
+  }
+  return 0;
+}
+
+// renorm_loose / finish on their own: in (count, W) levels -> out (count, W)
+int hst_lean_renorm_batch(int W, int finish, std::size_t count, const double* in, double* out) {
+  for (std::size_t c = 0; c < count; ++c) {
+    const double* x = in + c * W;
+    double* o = out + c * W;
+    if (W == 2) {
+      double s[2] = {x[0], x[1]};
+      if (finish) lean_finish<2>(s, o); else { lean_renorm_loose<2>(s); o[0] = s[0], o[1] = s[1]; }
+    } else if (W == 3) {
+      double s[3] = {x[0], x[1], x[2]};
+      if (finish) lean_finish<3>(s, o); else { lean_renorm_loose<3>(s); for (int w = 0; w < 3; ++w) o[w] = s[w]; }
+    } else if (W == 4) {
+      double s[4] = {x[0], x[1], x[2], x[3]};
+      if (finish) lean_finish<4>(s, o); else { lean_renorm_loose<4>(s); for (int w = 0; w < 4; ++w) o[w] = s[w]; }
+    } else {
+      return 1;
+    }
+  }
+  return 0;
+}
+
+// the lean GEMM on the host, element by element as the kernel runs it (plane
+// arrays like hst_gemm; k-tiles of 16)
+int hst_lean_gemm(int W, std::size_t m, std::size_t K, std::size_t n, const double* A, std::size_t lda,
+                  const double* B, std::size_t ldb, double* C, std::size_t ldc) {
+  const std::size_t pa = m * lda, pb = K * ldb, pc = m * ldc;
+  std::vector<double> a(K * W), b(K * W);
+  for (std::size_t i = 0; i < m; ++i)
+    for (std::size_t j = 0; j < n; ++j) {
+      for (std::size_t k = 0; k < K; ++k)
+        for (int w = 0; w < W; ++w) a[k * W + w] = A[w * pa + i * lda + k], b[k * W + w] = B[w * pb + k * ldb + j];
+      double o[4] = {0, 0, 0, 0};
+      if (W == 2) lean_dot<2>(K, a.data(), b.data(), 16, nullptr, o);
+      else if (W == 3) lean_dot<3>(K, a.data(), b.data(), 16, nullptr, o);
+      else if (W == 4) lean_dot<4>(K, a.data(), b.data(), 16, nullptr, o);
+      else return 1;
+      for (int w = 0; w < W; ++w) C[w * pc + i * ldc + j] = o[w];
+    }
+  return 0;
+}
+
+int hst_ref_dot_batch(int W, std::size_t count, std::size_t k, const double* a, const double* b, double* out) {
+  for (std::size_t c = 0; c < count; ++c) {
+    const double *x = a + c * k * W, *y = b + c * k * W;
+    double* o = out + c * W;
+    if (W == 2) ref_dot<2>(k, x, y, o);
+    else if (W == 3) ref_dot<3>(k, x, y, o);
+    else if (W == 4) ref_dot<4>(k, x, y, o);
+    else return 1;
+  }
+  return 0;
+}
 
 int hst_binop_batch(int W, int op, std::size_t count, const double* x, const double* y,
                     double* r) {
