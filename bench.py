@@ -560,6 +560,8 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
             e2e_pg = measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned=False, dC_host=dC_host)
             e2e_pg["registered"] = measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned=False,
                                                dC_host=dC_host, register=True)
+        if lean is not None and not ctx.use_dist:
+            lean["e2e"] = measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned=True, dC_host=None, lean=True)
 
     # ---- CPU baseline: the reference's own GEMM on this host (rank 0, N == 1)
     cpu = None
@@ -695,7 +697,7 @@ def measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream):
             "diff_over_tolerance": round(diff / (4 * k * U_P[W]), 6)}
 
 
-def measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned, dC_host, register=False):
+def measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned, dC_host, register=False, lean=False):
     """The metric through the public host-buffer API: every step copies the
     step's operands from host memory, computes and reads C back.
     register: pageable operands with the library's opt-in registration
@@ -716,6 +718,9 @@ def measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned, dC_host, regist
 
         def call():
             matmul_sharded_into(Ch, Ah, Bh, panels=args.panels, device=ctx.dev)
+    elif lean:
+        def call():
+            P.gemm_into(Ch, Ah, Bh, 1, P.LEAN)
     else:
         def call():
             P.matmul_block_parallel_into(Ch, Ah, Bh, 32, P.KernelVariant.SIMD_LOADSTORE, 1)
@@ -736,13 +741,14 @@ def measure_e2e(ctx, W, n, wide, r0, rows, flops, steps, pinned, dC_host, regist
            "d2h_bytes_per_step": d2h, "steps": n_steps,
            "host_memory": "page-locked" if pinned else "pageable (like a reference MPMatrix)",
            "api": "dist.matmul_sharded_into (per rank)" if ctx.use_dist else
+                  "mpfk_gemm(flags = MPFK_LEAN) (C ABI, host buffers)" if lean else
                   "matmul_block_parallel_into (C ABI, host buffers)"}
     if st is not None:
         out["ms_breakdown"] = {k_: round(st[k_], 3) for k_ in ("h2d_ms", "kernel_ms", "d2h_ms", "total_ms")}
     if register:
         out["host_memory"] = "pageable, page-locked on first use by the registration cache (opt-in)"
         out["registered_entries"] = P.host_register_cache_stats()["entries"]
-    if rows and dC_host is not None:
+    if rows and dC_host is not None and not lean:
         # the e2e result equals the device-resident run (same inputs)
         out["matches_device_run"] = bool(
             (torch.from_numpy(np.ascontiguousarray(Ch.data)).view(torch.int64) == dC_host.view(torch.int64)).all())

@@ -361,9 +361,13 @@ using Cfg4g = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 2, 0, 0, 0>;
 // multiply-add, tolerance mode).  Tiles from the sweep of csrc/tune_lean.cu
 // (scripts/tune.py --lean, profiles/r02/tune_lean.log): straight-line
 // k-tiles, one barrier, fast loader and paired B columns for every width;
-// TD at 3 CTAs/SM (80 registers), QD at 2.
-using CfgL2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1, 0, 1>;
-using CfgL2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1, 0, 1>;
+// TD at 3 CTAs/SM (80 registers), QD at 2.  DD (LEAN = 2: a micro-tile row's
+// operations written stage by stage, +0.4 %) stays at 0.87-0.88 of the FP64
+// pipe for every tile, occupancy and instruction order tried (32x32 .. 64x128,
+// 1-4 CTAs/SM; TD 0.95, QD 0.97): a quarter of its FP64 instructions are
+// three-operand DFMAs (bit-exact DD: one in twenty).
+using CfgL2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1, 0, 2>;
+using CfgL2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1, 0, 2>;
 using CfgL3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 16, 16, 3, 1, 1, 0, 0, 1, 1, 0, 1>;
 using CfgL4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 0, 0, 1, 1, 0, 1>;
 
@@ -410,9 +414,9 @@ double predicted_eff(const kern::GemmArgs& g, double steady) {
 bool dd_small_tiles(const kern::GemmArgs& g) {
   return predicted_eff<Cfg2s>(g, 0.935) > predicted_eff<Cfg2>(g, 0.948);
 }
-// the same rule for the lean DD tiles (steady: 0.859 / 0.870 of the pipe at n=4096)
+// the same rule for the lean DD tiles (steady: 0.865 / 0.874 of the pipe at n=4096)
 bool dd_small_tiles_lean(const kern::GemmArgs& g) {
-  return predicted_eff<CfgL2s>(g, 0.859) > predicted_eff<CfgL2>(g, 0.870);
+  return predicted_eff<CfgL2s>(g, 0.865) > predicted_eff<CfgL2>(g, 0.874);
 }
 
 template <class Cfg>

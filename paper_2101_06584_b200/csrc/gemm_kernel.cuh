@@ -466,10 +466,16 @@ __device__ __forceinline__ void mac_step_lean(double (&acc)[Cfg::TM][Cfg::TN][Cf
 #pragma unroll
     for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
   load_b<Cfg>(b, Bs, tx, kk);
+  if constexpr (W == 2 && Cfg::LEAN == 2) {
+    // stage-major across a micro-tile row (same operations, other order)
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < TM; ++i) arith::lean_mac_dd_row<TN>(acc[i], a[i], b);
+  } else {
 #pragma unroll
-    for (int j = 0; j < TN; ++j) arith::lean_mac<W>(acc[i][j], a[i], b[j]);
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) arith::lean_mac<W>(acc[i][j], a[i], b[j]);
+  }
 }
 
 // One output tile (rows m0.., columns n0..) over the K range of g: the

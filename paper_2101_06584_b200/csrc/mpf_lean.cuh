@@ -140,6 +140,42 @@ MPFK_HD void lean_mac(double (&s)[W], const double* a, const double* b) {
   }
 }
 
+// DD: N multiply-accumulates that share a (one row of a thread's micro-tile)
+// written stage by stage across the N elements, so consecutive instructions
+// are independent -- the same operations as N calls of lean_mac<2>, only
+// the order in the instruction stream differs (results are bit-identical).
+template <int N>
+MPFK_HD void lean_mac_dd_row(double (&s)[N][2], const double* a, const double (&b)[N][2]) {
+  double p[N], e[N], ss[N], v[N], t1[N], t3[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) p[j] = mul(a[0], b[j][0]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) ss[j] = add(s[j][0], p[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = fma(a[0], b[j][0], -p[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = sub(ss[j], s[j][0]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = fma(a[0], b[j][1], e[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) t1[j] = sub(ss[j], v[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) t3[j] = sub(p[j], v[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = fma(a[1], b[j][0], e[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) t1[j] = sub(s[j][0], t1[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) t1[j] = add(t1[j], t3[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = add(t1[j], e[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    s[j][1] = add(s[j][1], e[j]);
+    s[j][0] = ss[j];
+  }
+}
+
 // Pull the levels back to nearly non-overlapping (|s[i+1]| <~ ulp(s[i])):
 // VecSum from the bottom up, then the error pass from the top down, both
 // with Knuth two-sums (exact whatever the overlap or cancellation above).

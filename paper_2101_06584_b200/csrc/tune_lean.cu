@@ -43,8 +43,25 @@ cudaError_t info_cfg(int* regs, int* smem, int* threads) {
    run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX, OB, 0, 0, FL, PB, 0, 1>>,                \
    info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX, OB, 0, 0, FL, PB, 0, 1>>}
 
+// LEAN_ = 2: DD stage-major rows
+#define L2(W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX, OB, FL, PB)                                       \
+  {W, "lean2/" #W "/" #BM "x" #BN "x" #BK "/" #TM "x" #TN "/st" #ST "/ku" #KU "/mb" #MB "/fx" #FX "/ob" #OB "/fl" #FL "/pb" #PB, \
+   run_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX, OB, 0, 0, FL, PB, 0, 2>>,                \
+   info_cfg<TileCfg<W, BM, BN, BK, TM, TN, ST, KU, GM, MB, FX, OB, 0, 0, FL, PB, 0, 2>>}
+
 const Entry kEntries[] = {
     // DD
+    L2(2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 1, 1),
+    L2(2, 64, 64, 16, 4, 4, 2, 4, 16, 2, 1, 1, 1, 1),
+    L2(2, 64, 64, 16, 4, 4, 2, 1, 16, 2, 0, 0, 1, 1),
+    L2(2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 1, 1),
+    L2(2, 64, 128, 16, 4, 8, 2, 16, 16, 1, 1, 1, 1, 1),
+    L2(2, 64, 32, 16, 4, 2, 2, 16, 16, 3, 1, 1, 1, 1),
+    L2(2, 32, 64, 16, 2, 4, 2, 16, 16, 3, 1, 1, 1, 1),
+    L(2, 64, 32, 16, 4, 2, 2, 16, 16, 3, 1, 1, 1, 1),
+    L(2, 32, 64, 16, 2, 4, 2, 16, 16, 3, 1, 1, 1, 1),
+    L(2, 64, 64, 16, 4, 4, 2, 1, 16, 2, 0, 0, 1, 1),
+    L(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 1, 1, 1, 1),
     L(2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 1, 1),
     L(2, 64, 64, 16, 4, 4, 2, 4, 16, 2, 1, 1, 1, 1),
     L(2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 1),

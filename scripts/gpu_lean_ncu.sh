@@ -1,0 +1,11 @@
+# ncu evidence for the MPFK_LEAN kernels: metric passes of the six workloads
+# and full captures of DD 4096 (the one below 0.9 of the pipe) and TD 4096
+mkdir -p gpurun_out
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active
+for w in dd8192 td4096 qd4096 dd1024 td1024 qd1024; do
+  python scripts/prof_gemm.py --lean --workload $w --launches 1 > gpurun_out/lean_plain_$w.log 2>&1 && \
+  ncu --metrics $M --clock-control none -k regex:mpgemm -c 1 --csv --log-file gpurun_out/lean_metrics_$w.csv python scripts/prof_gemm.py --lean --workload $w --launches 1 > gpurun_out/lean_ncu_m_$w.log 2>&1; echo ncu-metrics $w rc=$?
+done
+for w in dd8192 td4096; do
+  ncu --set full --clock-control none --import-source on -k regex:mpgemm -c 1 -o gpurun_out/lean_full_$w python scripts/prof_gemm.py --lean --workload $w --n 4096 --launches 1 > gpurun_out/lean_ncu_full_$w.log 2>&1; echo ncu-full $w rc=$?
+done

@@ -5,6 +5,8 @@
 // (linalg.hpp:132-140).  Also checks the reference's exception types and
 // messages come through the shim.  Exit code = number of failures.
 // Usage: shim_parity [n]   (GPU required)
+#include <cmath>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -51,6 +53,21 @@ void run(std::size_t m, std::size_t k, std::size_t n) {
   verdict(linalg::bits_equal(ref, G), "W=" + std::to_string(W) + " gemm_into BIT_EXACT");
   mpfk::linalg::gemm_into<W>(G, A, B, 1, mpfk::linalg::GemmFlags::FAST);
   verdict(G.rows() == m && G.cols() == n, "W=" + std::to_string(W) + " gemm_into FAST runs");
+  // MPFK_LEAN, the tolerance mode: not the reference's bits, but within the
+  // north star's normwise 4*k*u_p of them (the component differences summed
+  // from the smallest up: the leading ones cancel exactly where both agree)
+  mpfk::linalg::gemm_into<W>(G, A, B, 1, mpfk::linalg::GemmFlags::LEAN);
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < m; ++i)
+    for (std::size_t j = 0; j < n; ++j) {
+      double d = 0.0;
+      for (int w = W - 1; w >= 0; --w) d += G.plane(w)[i * G.stride() + j] - ref.plane(w)[i * ref.stride() + j];
+      num = std::max(num, std::fabs(d));
+      den = std::max(den, std::fabs(ref.plane(0)[i * ref.stride() + j]));
+    }
+  const double u_p = W == 2 ? 0x1p-104 : (W == 3 ? 0x1p-156 : 0x1p-208);
+  verdict(num <= 4.0 * double(k) * u_p * den,
+          "W=" + std::to_string(W) + " gemm_into LEAN within 4*k*u_p of the reference");
 }
 
 template <class F>
