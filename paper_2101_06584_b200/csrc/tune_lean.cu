@@ -62,6 +62,15 @@ const Entry kEntries[] = {
     L(2, 32, 64, 16, 2, 4, 2, 16, 16, 3, 1, 1, 1, 1),
     L(2, 64, 64, 16, 4, 4, 2, 1, 16, 2, 0, 0, 1, 1),
     L(2, 64, 64, 16, 4, 4, 2, 2, 16, 2, 1, 1, 1, 1),
+    // fewer accumulators per thread at 2 CTAs/SM: registers left for interleaving
+    L(2, 64, 32, 16, 4, 2, 2, 16, 16, 2, 1, 1, 1, 1),
+    L2(2, 64, 32, 16, 4, 2, 2, 16, 16, 2, 1, 1, 1, 1),
+    L(2, 32, 64, 16, 2, 4, 2, 16, 16, 2, 1, 1, 1, 1),
+    L2(2, 32, 64, 16, 2, 4, 2, 16, 16, 2, 1, 1, 1, 1),
+    L2(2, 128, 32, 16, 8, 2, 2, 16, 16, 2, 1, 1, 1, 1),
+    L2(2, 32, 128, 16, 2, 8, 2, 16, 16, 2, 1, 1, 1, 1),
+    L2(2, 64, 64, 8, 4, 4, 2, 8, 16, 2, 1, 1, 1, 1),
+    L2(2, 64, 64, 32, 4, 4, 2, 32, 16, 2, 1, 1, 1, 1),
     L(2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 1, 1),
     L(2, 64, 64, 16, 4, 4, 2, 4, 16, 2, 1, 1, 1, 1),
     L(2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 1),

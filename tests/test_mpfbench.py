@@ -61,6 +61,16 @@ def test_matmul_and_ewise_runs(gpu_lib, tmp_path):
         if r["n"] == "16" and r["op"] != "strassen":
             assert float(r["max_rel_err"]) <= 16 * 4 * eps[r["precision"]]
             assert float(r["digits_lost"]) < 2.5
+    # the tolerance-mode variant: block rows only, its own error columns
+    out3 = tmp_path / "lean.csv"
+    assert MB.main(["matmul", "--sizes", "16,40", "--reps", "1", "--oracle-max", "40", "--algo", "block",
+                    "--variant", "gpu,gpu-lean", "--workers", "1,2", "--out", str(out3)]) == 0
+    rows3 = list(csv.DictReader(io.StringIO(out3.read_text())))
+    assert len(rows3) == 3 * 2 * 2 * 2
+    for r in rows3:
+        n3 = int(r["n"])
+        assert float(r["max_rel_err"]) <= n3 * 4 * eps[r["precision"]] * 8
+    assert {r["variant"] for r in rows3} == {"gpu", "gpu-lean"}
     out2 = tmp_path / "ew.csv"
     assert MB.main(["ewise", "--sizes", "64,4096", "--reps", "1", "--out", str(out2)]) == 0
     rows = list(csv.DictReader(io.StringIO(out2.read_text())))
