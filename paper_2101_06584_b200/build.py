@@ -58,6 +58,14 @@ def build_tune(force=False):
     return out
 
 
+def build_tune_lean(force=False):
+    """The MPFK_LEAN tile sweep library (scripts/tune.py --lean, TUNE_LIB); not the product."""
+    out = os.path.join(PKG, "libmpfk_tune_lean.so")
+    if force or _stale(out, _csrc_deps()):
+        _run([NVCC, *NVCC_FLAGS, "-shared", "-o", out, os.path.join(CSRC, "tune_lean.cu")])
+    return out
+
+
 def build_host_arith(force=False):
     outdir = os.path.join(ROOT, "tests", "_build")
     os.makedirs(outdir, exist_ok=True)
