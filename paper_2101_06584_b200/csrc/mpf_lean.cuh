@@ -45,7 +45,10 @@
 // accurate as the reference sequence, which renormalises after every
 // operation and lands at 4e-6 .. 2e-4 of the same tolerance (DD 2-4x, TD
 // 10-35x, QD 30-200x smaller errors than the lean form): the lean form
-// spends the tolerance the north star grants, it does not tighten it.
+// spends the tolerance the north star grants, it does not tighten it.  No
+// worst-case proof at 4*k*u_p is claimed (a bound with every rounding residual
+// of a k-tile aligned in sign exceeds it); DESIGN.md 9.2 lists what was
+// measured instead.
 //
 // finish() turns the levels into a canonical normalised value (what the
 // reference's renormalisation returns: each component at most half an ulp of
