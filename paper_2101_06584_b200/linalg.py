@@ -196,7 +196,10 @@ BIT_EXACT, FAST, LEAN = N.MPFK_BIT_EXACT, N.MPFK_FAST, N.MPFK_LEAN
 def gemm_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix, n_gpus: int = 1, flags: int = BIT_EXACT):
     """mpfk_gemm: C = A*B on n_gpus GPUs (<= 0: all).  flags=BIT_EXACT is
     matmul_block_parallel_into; flags=FAST may split K for outputs too small
-    to fill the GPU (deterministic, tolerance-checked: normwise 4*k*u_p)."""
+    to fill the GPU (deterministic, tolerance-checked: normwise 4*k*u_p);
+    flags=LEAN runs the tolerance-mode arithmetic (csrc/mpf_lean.cuh: 12 / 46 /
+    113 FP64 instructions per multiply-add, 1.5-2.5x the bit-exact rate, NOT
+    the reference's bits).  FAST | LEAN combines them."""
     W = _check_same_width(C_, A, B)
     c, a, b = C_._c(), A._c(), B._c()
     N.check(N.lib().mpfk_gemm(W, C.byref(a), C.byref(b), C.byref(c), int(n_gpus), int(flags)))
@@ -377,7 +380,8 @@ def gemm_device(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: i
 
 def gemm_device_ex(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int, ldb: int,
                    b_plane: int, C_ptr: int, ldc: int, c_plane: int, flags: int = BIT_EXACT, stream: int = 0) -> int:
-    """mpfk_gemm_device_ex: gemm_device with flags (FAST may split K)."""
+    """mpfk_gemm_device_ex: gemm_device with flags (FAST may split K, LEAN
+    selects the tolerance-mode arithmetic)."""
     launches = C.c_int(0)
     N.check(N.lib().mpfk_gemm_device_ex(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
                                         c_plane, int(flags), stream or None, C.byref(launches)))
