@@ -195,3 +195,19 @@ def test_lean_flags(gpu_lib):
     # k == 0: +0
     dC, _ = device_lean(P, W, A2, B2, m2, n2, 0, sentinel=3.0)
     assert np.all(dC[:, :, :n2] == 0)
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+def test_lean_paper_matrices_digit_loss(gpu_lib, W):
+    """acceptance criterion 5 (acceptance.cpp:286-337) for the tolerance mode:
+    the paper's generator matrices (exactly representable entries that drive
+    the reference's renorm5 paths B/C/D) lose at most 2.5 digits against the
+    exact product, componentwise, like the reference's own algorithms"""
+    P = gpu_lib
+    for n in (64, 256):
+        rows = (0, 8) if n == 256 else (0, n)
+        A, B = P.gen_paper_matrices(W, n)
+        exact = dyadic.matmul_exact(A.data, B.data, n, n, rows=rows)
+        Cm = P.gemm(A, B, flags=P.LEAN)
+        dl = dyadic.digit_loss(dyadic.max_rel_err(Cm.data, exact, rows=rows), P.format_eps(W))
+        assert dl <= 2.5, (n, dl)
