@@ -650,13 +650,13 @@ def describe_transport(transport, ws, args, note):
     return s + (f" [{note}]" if note else "")
 
 
-LEAN_OPS_PER_MAC = {2: 12 + 6 / 16, 3: 46 + 18 / 16, 4: 113 + 30 / 16}  # csrc/mpf_lean.cuh (+ renorm per 16-step k-tile)
+LEAN_OPS_PER_MAC = {2: 10 + 6 / 16, 3: 42 + 18 / 16, 4: 107 + 30 / 16}  # csrc/mpf_lean.cuh (+ renorm per 16-step k-tile)
 U_P = {2: 2.0 ** -104, 3: 2.0 ** -156, 4: 2.0 ** -208}  # north star
 
 
 def measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream):
     """The same device-resident GEMM with flags = MPFK_LEAN (the north star's
-    tolerance mode: 12 / 46 / 113 FP64 instructions per multiply-add instead
+    tolerance mode: 10 / 42 / 107 FP64 instructions per multiply-add instead
     of 20 / 119 / 218; NOT bit-identical to the reference).  Timed like the
     bit-exact steps; its result is compared with theirs (dC, bit-identical to
     the reference) as a normwise difference in units of 4*k*u_p."""

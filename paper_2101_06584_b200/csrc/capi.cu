@@ -357,7 +357,7 @@ using Cfg4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 2, 0, 0, 0>; 
 // n=4096 (e2e 891 vs 864 ms; the per-panel flag wait after the k-tile's
 // barrier is the culprit -- 4-step tiles with two barriers measure 867 ms)
 using Cfg4g = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 2, 0, 0, 0>;
-// MPFK_LEAN (csrc/mpf_lean.cuh: 12 / 46 / 113 FP64 instructions per
+// MPFK_LEAN (csrc/mpf_lean.cuh: 10 / 42 / 107 FP64 instructions per
 // multiply-add, tolerance mode).  Tiles from the sweep of csrc/tune_lean.cu
 // (scripts/tune.py --lean, profiles/r02/tune_lean.log): straight-line
 // k-tiles, one barrier, fast loader and paired B columns for every width;
@@ -367,7 +367,7 @@ using Cfg4g = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 1, 16, 2, 0, 0, 2, 0, 0, 0>;
 // 1-4 CTAs/SM; TD 0.95, QD 0.97): a quarter of its FP64 instructions are
 // three-operand DFMAs (bit-exact DD: one in twenty).
 using CfgL2 = kern::TileCfg<2, 64, 64, 16, 4, 4, 2, 16, 16, 2, 1, 1, 0, 0, 1, 1, 0, 2>;
-using CfgL2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1, 0, 2>;
+using CfgL2s = kern::TileCfg<2, 32, 32, 16, 2, 2, 2, 16, 16, 4, 1, 1, 0, 0, 1, 1, 0, 1>;  // (element-major: +2 % at n=1024)
 using CfgL3 = kern::TileCfg<3, 32, 32, 16, 2, 2, 2, 16, 16, 3, 1, 1, 0, 0, 1, 1, 0, 1>;
 using CfgL4 = kern::TileCfg<4, 32, 32, 16, 2, 2, 2, 4, 16, 2, 1, 1, 0, 0, 1, 1, 0, 1>;
 

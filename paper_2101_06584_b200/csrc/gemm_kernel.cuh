@@ -107,7 +107,7 @@ struct TileCfg {
   // MPFK_LEAN (mpf_lean.cuh): the tolerance-mode multiply-accumulate --
   // every element is W levels fed by exact two-sum cascades, pulled back to
   // nearly non-overlapping once per k-tile and normalised once at the end.
-  // 12 / 46 / 113 FP64 instructions per step; NOT bit-identical to the
+  // 10 / 42 / 107 FP64 instructions per step; NOT bit-identical to the
   // reference (within the north star's 4*k*u_p).  No data-dependent path, so
   // no FASTR machinery.
   static constexpr int LEAN = LEAN_;

@@ -1,5 +1,5 @@
 // mpf_lean.cuh -- the MPFK_LEAN multiply-accumulate: C += a*b for DD/TD/QD
-// with 12 / 46 / 113 FP64 operations instead of the reference sequence's
+// with 10 / 42 / 107 FP64 operations instead of the reference sequence's
 // 20 / 119 (132 counted) / 218.
 //
 // NOT the reference's arithmetic and NOT bit-identical to it: this is the
@@ -30,25 +30,27 @@
 //     x moves on to level L+1, ..., and what reaches the last level is added
 //     in plain binary64.
 //
+//   * a product of the next-to-last order does not get a separate two_prod
+//     error and two-sum error: both belong to the last level, and one fma
+//     forms their sum in a single rounding (lean_last_prod; for DD this is
+//     the leading product itself, lean_mac<2>).
+//
 // Every operation above the last level is exact, so the only rounding errors
-// are the plain additions at the last level (each at most u * |s[W-1]|) and
-// the dropped product terms of order >= W (the same ones the reference
-// drops).  |s[W-1]| is held near u^(W-1) * |C| by renorm_loose() once per
-// k-tile (16 steps), so each step's error is a small multiple of u^W * |C|:
-//   DD  2 last-level adds/step, dropped/rounded product terms ~3 u^2 |a||b|
-//   TD  5 last-level adds/step, ~3.5 u^3 |a||b|
-//   QD 10 last-level adds/step, ~7 u^4 |a||b|
-// against a budget of 4*u_p = 16 u^2 / 32 u^3 / 64 u^4 per step (u = 2^-53,
-// u_p = 2^-104 / 2^-156 / 2^-208).  Measured against the exact dyadic oracle
-// (tests/test_lean_host.py, tests/test_lean_gpu.py) on the BASELINE
-// distributions at k = 2048..4096: 2e-4 .. 1.5e-3 of 4*k*u_p.  That is NOT as
-// accurate as the reference sequence, which renormalises after every
-// operation and lands at 4e-6 .. 2e-4 of the same tolerance (DD 2-4x, TD
-// 10-35x, QD 30-200x smaller errors than the lean form): the lean form
-// spends the tolerance the north star grants, it does not tighten it.  No
-// worst-case proof at 4*k*u_p is claimed (a bound with every rounding residual
-// of a k-tile aligned in sign exceeds it); DESIGN.md 9.2 lists what was
-// measured instead.
+// are the plain additions and fused corrections at the last level (each at
+// most u * |s[W-1]| resp. u * ulp(s[W-2])) and the dropped product terms of
+// order >= W (the same ones the reference drops).  |s[W-1]| is held near
+// u^(W-1) * |C| by renorm_loose() once per k-tile (16 steps), so each step's
+// error is a small multiple of u^W * |C| against a budget of 4*u_p = 16 u^2 /
+// 32 u^3 / 64 u^4 per step (u = 2^-53, u_p = 2^-104 / 2^-156 / 2^-208).
+// Measured against the exact dyadic oracle (tests/test_lean_host.py,
+// tests/test_lean_gpu.py) on the BASELINE distributions at k = 2048..4096:
+// 2e-4 .. 1.5e-3 of 4*k*u_p.  That is NOT as accurate as the reference
+// sequence, which renormalises after every operation and lands at 4e-6 ..
+// 2e-4 of the same tolerance (DD 1-3x, TD 14-72x, QD 36-290x smaller errors
+// than the lean form): the lean form spends the tolerance the north star
+// grants, it does not tighten it.  No worst-case proof at 4*k*u_p is claimed
+// (a bound with every rounding residual of a k-tile aligned in sign exceeds
+// it); DESIGN.md 9.2 lists what was measured instead.
 //
 // finish() turns the levels into a canonical normalised value (what the
 // reference's renormalisation returns: each component at most half an ulp of
@@ -67,7 +69,7 @@ namespace arith {
 // +30/16).
 template <int W>
 constexpr int lean_ops_per_mac() {
-  return W == 2 ? 12 : (W == 3 ? 46 : 113);
+  return W == 2 ? 10 : (W == 3 ? 42 : 107);
 }
 template <int W>
 constexpr int lean_renorm_ops() {
@@ -88,58 +90,80 @@ MPFK_HD double lean_cascade(double (&s)[W], double x) {
   return x;
 }
 
+// A product x*y of the next-to-last order enters its level sl (the last one
+// fed by two-sums): sl' = sl + p with p = RN(x*y).  Knuth's two-sum error is
+// t2 + (p - v) (v = sl' - sl, t2 = sl - (sl' - v)) and the product's own
+// error is x*y - p; both belong to the last level, where additions are plain
+// anyway, so they are formed together: fma(x, y, -v) = (x*y - p) + (p - v) in
+// one rounding (error <= u * |x*y - v|, of the last level's order times u).
+// Returns what goes to the last level.  7 operations instead of 10.
+MPFK_HD double lean_last_prod(double& sl, double x, double y) {
+  const double p = mul(x, y);
+  const double ss = add(sl, p);
+  const double v = sub(ss, sl);
+  const double t2 = sub(sl, sub(ss, v));
+  const double g = fma(x, y, -v);
+  sl = ss;
+  return add(t2, g);
+}
+
 // s += a * b (a, b normalised W-term values; s the levels)
 template <int W>
 MPFK_HD void lean_mac(double (&s)[W], const double* a, const double* b) {
   if constexpr (W == 2) {
-    // order 0: p; order 1: its error and the cross products, one fma chain
+    // 10 operations.  Knuth's two-sum of (s0, p) is ss = s0 + p with the
+    // exact error t2 + (p - v) (v = ss - s0, t2 = s0 - (ss - v)); the exact
+    // product is p + (a0*b0 - p).  The two corrections are not formed one by
+    // one: g = fma(a0, b0, -v) is (a0*b0 - p) + (p - v) in ONE rounding
+    // (error <= u*|a0*b0 - v| <= u^2 (|p| + |ss|), second order like the
+    // dropped a1*b1), and the cross products join the same fma chain.
     const double p = mul(a[0], b[0]);
-    double e = fma(a[0], b[0], -p);
-    e = fma(a[0], b[1], e);
-    e = fma(a[1], b[0], e);
-    const double r = lean_cascade<2, 0>(s, p);
-    s[1] = add(s[1], add(r, e));
+    const double ss = add(s[0], p);
+    const double v = sub(ss, s[0]);
+    const double t2 = sub(s[0], sub(ss, v));
+    double g = fma(a[0], b[0], -v);
+    g = fma(a[0], b[1], g);
+    g = fma(a[1], b[0], g);
+    s[1] = add(s[1], add(t2, g));
+    s[0] = ss;
   } else if constexpr (W == 3) {
+    // 42 operations: order 0 exactly through s0, s1; its error exactly
+    // through s1; the order-1 products through s1 with the fused correction
+    // (lean_last_prod); order 2 in plain binary64
+    double p00, e00;
+    two_prod(a[0], b[0], p00, e00);
+    double t = mul(a[0], b[2]);
+    t = fma(a[1], b[1], t);
+    t = fma(a[2], b[0], t);
+    const double r0 = lean_cascade<3, 0>(s, p00);
+    const double r1 = lean_cascade<3, 1>(s, e00);
+    const double q01 = lean_last_prod(s[1], a[0], b[1]);
+    const double q10 = lean_last_prod(s[1], a[1], b[0]);
+    s[2] = add(s[2], add(add(add(r0, r1), add(q01, q10)), t));
+  } else {
+    // 107 operations: orders 0 and 1 exactly (two_prod errors included)
+    // through every level above the last; the order-2 products through s2
+    // with the fused correction; order 3 in plain binary64
     double p00, e00, p01, e01, p10, e10;
     two_prod(a[0], b[0], p00, e00);
     two_prod(a[0], b[1], p01, e01);
     two_prod(a[1], b[0], p10, e10);
-    // order 2 in plain binary64
-    double t = mul(a[0], b[2]);
-    t = fma(a[1], b[1], t);
-    t = fma(a[2], b[0], t);
-    t = add(t, add(e01, e10));
-    const double r0 = lean_cascade<3, 0>(s, p00);
-    const double r1 = lean_cascade<3, 1>(s, e00);
-    const double r2 = lean_cascade<3, 1>(s, p01);
-    const double r3 = lean_cascade<3, 1>(s, p10);
-    s[2] = add(s[2], add(add(add(r0, r1), add(r2, r3)), t));
-  } else {
-    double p00, e00, p01, e01, p10, e10, p02, e02, p11, e11, p20, e20;
-    two_prod(a[0], b[0], p00, e00);
-    two_prod(a[0], b[1], p01, e01);
-    two_prod(a[1], b[0], p10, e10);
-    two_prod(a[0], b[2], p02, e02);
-    two_prod(a[1], b[1], p11, e11);
-    two_prod(a[2], b[0], p20, e20);
-    // order 3 in plain binary64
     double t = mul(a[0], b[3]);
     t = fma(a[1], b[2], t);
     t = fma(a[2], b[1], t);
     t = fma(a[3], b[0], t);
-    t = add(t, add(add(e02, e11), e20));
     const double r0 = lean_cascade<4, 0>(s, p00);
     const double r1 = lean_cascade<4, 1>(s, e00);
     const double r2 = lean_cascade<4, 1>(s, p01);
     const double r3 = lean_cascade<4, 1>(s, p10);
     const double r4 = lean_cascade<4, 2>(s, e01);
     const double r5 = lean_cascade<4, 2>(s, e10);
-    const double r6 = lean_cascade<4, 2>(s, p02);
-    const double r7 = lean_cascade<4, 2>(s, p11);
-    const double r8 = lean_cascade<4, 2>(s, p20);
+    const double q02 = lean_last_prod(s[2], a[0], b[2]);
+    const double q11 = lean_last_prod(s[2], a[1], b[1]);
+    const double q20 = lean_last_prod(s[2], a[2], b[0]);
     const double ra = add(add(r0, r1), add(r2, r3));
-    const double rb = add(add(r4, r5), add(r6, r7));
-    s[3] = add(s[3], add(add(ra, rb), add(r8, t)));
+    const double rb = add(add(r4, r5), add(q02, q11));
+    s[3] = add(s[3], add(add(ra, rb), add(q20, t)));
   }
 }
 
@@ -149,32 +173,28 @@ MPFK_HD void lean_mac(double (&s)[W], const double* a, const double* b) {
 // the order in the instruction stream differs (results are bit-identical).
 template <int N>
 MPFK_HD void lean_mac_dd_row(double (&s)[N][2], const double* a, const double (&b)[N][2]) {
-  double p[N], e[N], ss[N], v[N], t1[N], t3[N];
+  double p[N], ss[N], v[N], t[N], g[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) p[j] = mul(a[0], b[j][0]);
 #pragma unroll
   for (int j = 0; j < N; ++j) ss[j] = add(s[j][0], p[j]);
 #pragma unroll
-  for (int j = 0; j < N; ++j) e[j] = fma(a[0], b[j][0], -p[j]);
-#pragma unroll
   for (int j = 0; j < N; ++j) v[j] = sub(ss[j], s[j][0]);
 #pragma unroll
-  for (int j = 0; j < N; ++j) e[j] = fma(a[0], b[j][1], e[j]);
+  for (int j = 0; j < N; ++j) t[j] = sub(ss[j], v[j]);
 #pragma unroll
-  for (int j = 0; j < N; ++j) t1[j] = sub(ss[j], v[j]);
+  for (int j = 0; j < N; ++j) g[j] = fma(a[0], b[j][0], -v[j]);
 #pragma unroll
-  for (int j = 0; j < N; ++j) t3[j] = sub(p[j], v[j]);
+  for (int j = 0; j < N; ++j) t[j] = sub(s[j][0], t[j]);
 #pragma unroll
-  for (int j = 0; j < N; ++j) e[j] = fma(a[1], b[j][0], e[j]);
+  for (int j = 0; j < N; ++j) g[j] = fma(a[0], b[j][1], g[j]);
 #pragma unroll
-  for (int j = 0; j < N; ++j) t1[j] = sub(s[j][0], t1[j]);
+  for (int j = 0; j < N; ++j) g[j] = fma(a[1], b[j][0], g[j]);
 #pragma unroll
-  for (int j = 0; j < N; ++j) t1[j] = add(t1[j], t3[j]);
-#pragma unroll
-  for (int j = 0; j < N; ++j) e[j] = add(t1[j], e[j]);
+  for (int j = 0; j < N; ++j) g[j] = add(t[j], g[j]);
 #pragma unroll
   for (int j = 0; j < N; ++j) {
-    s[j][1] = add(s[j][1], e[j]);
+    s[j][1] = add(s[j][1], g[j]);
     s[j][0] = ss[j];
   }
 }

@@ -25,7 +25,7 @@ ap.add_argument("--lean", action="store_true",
                 help="MPFK_LEAN entries (TUNE_LIB=libmpfk_tune_lean.so): compared with the bit-exact product within "
                      "4*k*u_p (normwise), fractions in executed FP64 instructions")
 a = ap.parse_args()
-LEAN_OPS = {2: 12 + 6 / 16, 3: 46 + 18 / 16, 4: 113 + 30 / 16}  # mpf_lean.cuh, renorm_loose per 16-step k-tile
+LEAN_OPS = {2: 10 + 6 / 16, 3: 42 + 18 / 16, 4: 107 + 30 / 16}  # mpf_lean.cuh, renorm_loose per 16-step k-tile
 U_P = {2: 2.0 ** -104, 3: 2.0 ** -156, 4: 2.0 ** -208}
 
 
