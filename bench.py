@@ -534,8 +534,9 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
         check = min(ctx.gather_float(1.0 if ok else 0.0)) == 1.0
 
     lean = None
-    if ws == 1 and rows and not args.no_lean and transport not in ("nccl", "bcast"):
-        lean = measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream)
+    if not args.no_lean and ((ws == 1 and rows and slices is None and transport not in ("nccl", "bcast")) or
+                             (slices is not None and transport == "staged")):
+        lean = measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream, slices=slices)
 
     step_ms = [a.elapsed_time(c) for a, _, c in evs]
     kern_ms = [b.elapsed_time(c) for _, b, c in evs]
@@ -620,7 +621,7 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
     if lean is not None:
         lean["frac_executed"] = round(rows * n * k * lean["ops_per_mac_executed"] /
                                       (lean["ms_per_step"] * 1e-3) / 1e9 / peak, 4)
-        lean["speedup_vs_bit_exact"] = round(t_kern / lean["ms_per_step"], 3)
+        lean["speedup_vs_bit_exact"] = round((t_step if ctx.use_dist else t_kern) / lean["ms_per_step"], 3)
         rec["lean"] = lean
     if e2e_pg is not None:
         rec["e2e_pageable"] = e2e_pg
@@ -654,21 +655,27 @@ LEAN_OPS_PER_MAC = {2: 10 + 6 / 16, 3: 42 + 18 / 16, 4: 107 + 30 / 16}  # csrc/m
 U_P = {2: 2.0 ** -104, 3: 2.0 ** -156, 4: 2.0 ** -208}  # north star
 
 
-def measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream):
+def measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream, slices=None):
     """The same device-resident GEMM with flags = MPFK_LEAN (the north star's
     tolerance mode: 10 / 42 / 107 FP64 instructions per multiply-add instead
     of 20 / 119 / 218; NOT bit-identical to the reference).  Timed like the
-    bit-exact steps; its result is compared with theirs (dC, bit-identical to
-    the reference) as a normwise difference in units of 4*k*u_p."""
-    torch, P = ctx.torch, ctx.P
+    bit-exact steps (N > 1: the staged all-gather -> GEMM of every rank's
+    shard, max over ranks); its result is compared with theirs (dC,
+    bit-identical to the reference) as a normwise difference in units of
+    4*k*u_p."""
+    torch, P, args = ctx.torch, ctx.P, ctx.args
     dL = torch.zeros_like(dC)
 
     def step():
+        if slices is not None:
+            return slices.step(W, dA, dB, dL, rows, n, k, args.pull_panel, args.pull_chunk, stream, mode="staged",
+                               flags=P.LEAN)
         return P.gemm_device_ex(W, rows, n, k, dA.data_ptr(), ld, rows * ld, dB.data_ptr(), ld, k * ld,
                                 dL.data_ptr(), ld, rows * ld, P.LEAN, stream.cuda_stream)
     for _ in range(2):
         step()
     torch.cuda.synchronize(ctx.dev)
+    ctx.barrier()
     n_steps = max(2, min(steps, 5))
     evs = []
     for _ in range(n_steps):
@@ -680,16 +687,23 @@ def measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream):
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize(ctx.dev)
-    t = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+    ctx.barrier()
+    t_local = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
     # sum the component differences from the smallest up: the leading
     # components cancel exactly where the two results agree
-    d = dL[W - 1] - dC[W - 1]
-    for w in range(W - 2, -1, -1):
-        d = d + (dL[w] - dC[w])
-    diff = float(d[:, :n].abs().max() / dC[0][:, :n].abs().max())
-    del dL, d
+    num = den = 0.0
+    if rows:
+        d = dL[W - 1] - dC[W - 1]
+        for w in range(W - 2, -1, -1):
+            d = d + (dL[w] - dC[w])
+        num, den = float(d[:rows, :n].abs().max()), float(dC[0][:rows, :n].abs().max())
+        del d
+    del dL
+    t, num, den = ctx.max_over_ranks([t_local, num, den])
+    diff = num / den if den else 0.0
+    m_total = n  # square workloads: all ranks' rows
     return {"flags": "MPFK_LEAN (tolerance mode; not bit-identical to the reference)",
-            "value": round(2.0 * rows * n * k / (t * 1e-3) / 1e9, 3), "unit": "Gflop/s",
+            "value": round(2.0 * m_total * n * k / (t * 1e-3) / 1e9, 3), "unit": "Gflop/s",
             "ms_per_step": round(t, 3), "steps": n_steps,
             "ops_per_mac_executed": LEAN_OPS_PER_MAC[W],
             "normwise_diff_vs_bit_exact": diff,

@@ -201,6 +201,14 @@ int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const do
                          uint64_t lda, uint64_t a_plane, const double *B, uint64_t ldb,
                          uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, void *stream,
                          int *launches);
+/* ... with flags: MPFK_BIT_EXACT, or MPFK_LEAN -- the tolerance-mode
+ * arithmetic continues from the normalised value in C (each panel ends with
+ * the lean form's final normalisation, so a panelled product is within the
+ * tolerance of, not bit-identical to, the one-shot lean product). */
+int mpfk_gemm_device_acc_ex(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                            uint64_t lda, uint64_t a_plane, const double *B, uint64_t ldb,
+                            uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane,
+                            unsigned flags, void *stream, int *launches);
 
 /* Fused all-gather -> GEMM in ONE kernel: B is not resident on this device;
  * its rows [src_row0[s], src_row0[s+1]) live in source slice s (nsrc <= 8),
@@ -249,6 +257,13 @@ int mpfk_gemm_device_staged(int width, uint64_t m, uint64_t n, uint64_t k, const
                             uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, int nsrc,
                             const double *const *src, const uint64_t *src_row0,
                             uint64_t head_rows, void *stream, int *launches);
+/* ... with flags: MPFK_BIT_EXACT, or MPFK_LEAN (every panel's launch in the
+ * tolerance-mode arithmetic; deterministic for a given panel schedule). */
+int mpfk_gemm_device_staged_ex(int width, uint64_t m, uint64_t n, uint64_t k, const double *A,
+                               uint64_t lda, uint64_t a_plane, double *B, uint64_t ldb,
+                               uint64_t b_plane, double *C, uint64_t ldc, uint64_t c_plane, int nsrc,
+                               const double *const *src, const uint64_t *src_row0,
+                               uint64_t head_rows, unsigned flags, void *stream, int *launches);
 /* device memory and CUDA IPC plumbing for the fused path (one process per
  * GPU): handles are 64-byte cudaIpcMemHandle_t blobs. */
 int mpfk_device_alloc(uint64_t bytes, void **ptr);

@@ -90,6 +90,11 @@ _SIGS = {
     "mpfk_mpfm_save_host": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(MpfkMat)]),
     "mpfk_gemm_device_acc": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                        _U64, _P, C.POINTER(C.c_int)]),
+    "mpfk_gemm_device_acc_ex": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
+                                          _U64, C.c_uint, _P, C.POINTER(C.c_int)]),
+    "mpfk_gemm_device_staged_ex": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
+                                             _U64, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_U64), _U64, C.c_uint,
+                                             _P, C.POINTER(C.c_int)]),
     "mpfk_gemm_device_pull": (C.c_int, [C.c_int, _U64, _U64, _U64, _P, _U64, _U64, _P, _U64, _U64, _P, _U64,
                                         _U64, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_U64), _U64, _U64, _P,
                                         C.POINTER(C.c_int)]),

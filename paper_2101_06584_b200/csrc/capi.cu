@@ -1306,8 +1306,17 @@ int mpfk_ew_device(int width, int op, uint64_t rows, uint64_t cols, double* out,
 int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
                          uint64_t a_plane, const double* B, uint64_t ldb, uint64_t b_plane, double* C,
                          uint64_t ldc, uint64_t c_plane, void* stream, int* launches) {
+  return mpfk_gemm_device_acc_ex(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, MPFK_BIT_EXACT,
+                                 stream, launches);
+}
+
+int mpfk_gemm_device_acc_ex(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                            uint64_t a_plane, const double* B, uint64_t ldb, uint64_t b_plane, double* C,
+                            uint64_t ldc, uint64_t c_plane, unsigned flags, void* stream, int* launches) {
   return guarded([&] {
     check_width(width);
+    // a continuation is one launch over this panel: MPFK_FAST (split K) has no meaning here
+    if (flags & ~unsigned(MPFK_LEAN)) fail(MPFK_EINVAL, "mpfk: a K-panel continuation takes MPFK_LEAN only");
     if (lda < k || ldb < n || ldc < n) fail(MPFK_EINVAL, "mpfk: leading dimension too small");
     if ((lda | ldb | ldc | a_plane | b_plane | c_plane) & 1)
       fail(MPFK_EINVAL, "mpfk: device strides must be even (16-byte rows)");
@@ -1317,7 +1326,7 @@ int mpfk_gemm_device_acc(int width, uint64_t m, uint64_t n, uint64_t k, const do
     const int dev = current_device();
     ensure_devices(1, dev);
     const int l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane,
-                               static_cast<cudaStream_t>(stream), true);
+                               static_cast<cudaStream_t>(stream), true, (flags & MPFK_LEAN) != 0);
     if (k) {  // k more multiply-adds per element: k muls and k adds
       tally_muls(m * n * k);
       tally_adds(m * n * k);
@@ -1551,8 +1560,19 @@ int mpfk_gemm_device_staged(int width, uint64_t m, uint64_t n, uint64_t k, const
                             uint64_t a_plane, double* B, uint64_t ldb, uint64_t b_plane, double* C, uint64_t ldc,
                             uint64_t c_plane, int nsrc, const double* const* src, const uint64_t* src_row0,
                             uint64_t head_rows, void* stream, int* launches) {
+  return mpfk_gemm_device_staged_ex(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, nsrc, src,
+                                    src_row0, head_rows, MPFK_BIT_EXACT, stream, launches);
+}
+
+int mpfk_gemm_device_staged_ex(int width, uint64_t m, uint64_t n, uint64_t k, const double* A, uint64_t lda,
+                               uint64_t a_plane, double* B, uint64_t ldb, uint64_t b_plane, double* C,
+                               uint64_t ldc, uint64_t c_plane, int nsrc, const double* const* src,
+                               const uint64_t* src_row0, uint64_t head_rows, unsigned flags, void* stream,
+                               int* launches) {
   return guarded([&] {
     check_width(width);
+    if (flags & ~unsigned(MPFK_LEAN)) fail(MPFK_EINVAL, "mpfk: the staged all-gather GEMM takes MPFK_LEAN only");
+    const bool lean = (flags & MPFK_LEAN) != 0;
     check_device_operands(n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane);
     const int dev = current_device();
     ensure_devices(1, dev);
@@ -1565,7 +1585,7 @@ int mpfk_gemm_device_staged(int width, uint64_t m, uint64_t n, uint64_t k, const
     int l = 0;
     if (!(m && n && k)) {
       if (n && k) S.copy(width, B, ldb, b_plane, 0, k, s, -1);
-      l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, s);
+      l = enqueue_gemm(width, m, n, k, A, lda, a_plane, B, ldb, b_plane, C, ldc, c_plane, s, false, lean);
     } else {
       // the gather runs on the device's gather stream -- peer slices on the
       // copy engines over NVLink -- in ascending K panels, one event per
@@ -1584,7 +1604,7 @@ int mpfk_gemm_device_staged(int width, uint64_t m, uint64_t n, uint64_t k, const
       for (int p = 0; p < np; ++p) {
         ck(cudaStreamWaitEvent(s, D.evS[p + 1], 0), "wait panel");
         l += enqueue_gemm(width, m, n, cut[p + 1] - cut[p], A + cut[p], lda, a_plane, B + cut[p] * ldb, ldb,
-                          b_plane, C, ldc, c_plane, s, p > 0);
+                          b_plane, C, ldc, c_plane, s, p > 0, lean);
       }
     }
     count_matmul(m, n, k);

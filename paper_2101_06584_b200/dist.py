@@ -291,7 +291,8 @@ class PeerBSlices:
         if a.size:
             L.memcpy(self.local, a.ctypes.data, a.nbytes)
 
-    def step(self, W, dA, dB, dC, rows, n, k, panel_rows=256, chunk_rows=2, stream=None, mode="pull") -> int:
+    def step(self, W, dA, dB, dC, rows, n, k, panel_rows=256, chunk_rows=2, stream=None, mode="pull",
+             flags=0) -> int:
         """C_shard = A_shard * B with B gathered from the slices while the GEMM
         computes: mode "staged" -- the copy engines gather B in growing K
         panels and one GEMM launch per panel waits on that panel's event
@@ -307,7 +308,9 @@ class PeerBSlices:
         if mode == "staged":
             return L.gemm_device_staged(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
                                         dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, self.ptrs,
-                                        self.cuts, 0, s)
+                                        self.cuts, 0, s, flags)
+        if flags:
+            raise ValueError("PeerBSlices.step: flags (MPFK_LEAN) need mode 'staged'")
         if mode == "copy":
             return L.gemm_device_gathered(W, rows, n, k, dA.data_ptr(), lda, dA.shape[1] * lda, dB.data_ptr(), ldb,
                                           dB.shape[1] * ldb, dC.data_ptr(), ldc, dC.shape[1] * ldc, self.ptrs,

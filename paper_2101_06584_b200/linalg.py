@@ -389,11 +389,13 @@ def gemm_device_ex(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane
 
 
 def gemm_device_acc(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int, ldb: int,
-                    b_plane: int, C_ptr: int, ldc: int, c_plane: int, stream: int = 0) -> int:
-    """Continue the chains in C over one K panel (mpfk_gemm_device_acc)."""
+                    b_plane: int, C_ptr: int, ldc: int, c_plane: int, stream: int = 0,
+                    flags: int = BIT_EXACT) -> int:
+    """Continue the chains in C over one K panel (mpfk_gemm_device_acc[_ex];
+    flags: BIT_EXACT or LEAN)."""
     launches = C.c_int(0)
-    N.check(N.lib().mpfk_gemm_device_acc(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
-                                         c_plane, stream or None, C.byref(launches)))
+    N.check(N.lib().mpfk_gemm_device_acc_ex(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
+                                            c_plane, int(flags), stream or None, C.byref(launches)))
     return launches.value
 
 
@@ -529,17 +531,18 @@ def gemm_device_gathered(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a
 
 def gemm_device_staged(W: int, m: int, n: int, k: int, A_ptr: int, lda: int, a_plane: int, B_ptr: int,
                        ldb: int, b_plane: int, C_ptr: int, ldc: int, c_plane: int, src_ptrs, src_row0,
-                       head_rows: int = 0, stream: int = 0) -> int:
+                       head_rows: int = 0, stream: int = 0, flags: int = BIT_EXACT) -> int:
     """All-gather -> GEMM with the copy engines gathering B's K panels from
     the source slices and one GEMM launch per panel gated on that panel's
-    event (mpfk_gemm_device_staged); B_ptr receives the whole B."""
+    event (mpfk_gemm_device_staged[_ex]; flags: BIT_EXACT or LEAN); B_ptr
+    receives the whole B."""
     ns = len(src_ptrs)
     srcs = (C.c_void_p * ns)(*src_ptrs)
     rows = (C.c_uint64 * (ns + 1))(*src_row0)
     launches = C.c_int(0)
-    N.check(N.lib().mpfk_gemm_device_staged(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
-                                            c_plane, ns, srcs, rows, head_rows, stream or None,
-                                            C.byref(launches)))
+    N.check(N.lib().mpfk_gemm_device_staged_ex(W, m, n, k, A_ptr, lda, a_plane, B_ptr, ldb, b_plane, C_ptr, ldc,
+                                               c_plane, ns, srcs, rows, head_rows, int(flags), stream or None,
+                                               C.byref(launches)))
     return launches.value
 
 

@@ -55,6 +55,11 @@ def test_torchrun_fused_allgather_path(gpu_lib, mode, launches):
     assert line["check_sharded_equals_one_shot"] is True  # the default with a process group
     assert line["gpu_launches"] == 2 * launches
     assert {"copy": "gathered", "pull": "device_pull", "staged": "device_staged"}[mode] in line["transport"]
+    if mode == "staged":  # the tolerance-mode leg rides the same transport (mpfk_gemm_device_staged_ex)
+        assert line["lean"]["value"] > line["value"]
+        assert 0 < line["lean"]["diff_over_tolerance"] <= 0.05
+    else:
+        assert "lean" not in line
 
 
 @pytest.mark.gpu

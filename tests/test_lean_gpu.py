@@ -211,3 +211,53 @@ def test_lean_paper_matrices_digit_loss(gpu_lib, W):
         Cm = P.gemm(A, B, flags=P.LEAN)
         dl = dyadic.digit_loss(dyadic.max_rel_err(Cm.data, exact, rows=rows), P.format_eps(W))
         assert dl <= 2.5, (n, dl)
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+def test_lean_k_panels_and_staged_gather(gpu_lib, W):
+    """MPFK_LEAN through the K-panel continuation (mpfk_gemm_device_acc_ex) and
+    the staged all-gather -> GEMM (mpfk_gemm_device_staged_ex): the staged
+    call equals its panel schedule replayed by hand, bitwise; a panelled lean
+    product is within the tolerance of the bit-exact one (each panel ends
+    with the lean form's normalisation, so it is not the one-shot chain)."""
+    import torch
+    from tests.test_staged_gpu import expected_panels
+    P = gpu_lib
+    m, k, n = 70, 1000, 66
+    cuts = [0, 1, 100, 500, 930, 1000]
+    A = O.orc_fill_baseline(W, m, k, 41, wide=True)
+    B = O.orc_fill_baseline(W, k, n, 42, wide=True)
+    ld = B.shape[2]
+    dA, dBfull = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    slices = [torch.from_numpy(np.ascontiguousarray(B[:, r0:r1])).cuda() for r0, r1 in zip(cuts, cuts[1:])]
+    dB = torch.full((W, k, ld), float("nan"), dtype=torch.float64, device="cuda")
+    dC = torch.full((W, m, ld), 7.0, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        launches = P.gemm_device_staged(W, m, n, k, dA.data_ptr(), A.shape[2], m * A.shape[2], dB.data_ptr(), ld,
+                                        k * ld, dC.data_ptr(), ld, m * ld, [t.data_ptr() for t in slices], cuts,
+                                        16, s.cuda_stream, flags=P.LEAN)
+    s.synchronize()
+    panels = expected_panels(k, 16)
+    assert launches == len(panels) - 1
+    assert np.array_equal(dB.cpu().numpy().view(np.uint64), B.view(np.uint64))
+    # the same schedule by hand
+    dH = torch.zeros((W, m, ld), dtype=torch.float64, device="cuda")
+    for p, (k0, k1) in enumerate(zip(panels, panels[1:])):
+        a_ptr, b_ptr = dA.data_ptr() + 8 * k0, dBfull.data_ptr() + 8 * k0 * ld
+        if p == 0:
+            P.gemm_device_ex(W, m, n, k1 - k0, a_ptr, A.shape[2], m * A.shape[2], b_ptr, ld, k * ld, dH.data_ptr(),
+                             ld, m * ld, P.LEAN)
+        else:
+            P.gemm_device_acc(W, m, n, k1 - k0, a_ptr, A.shape[2], m * A.shape[2], b_ptr, ld, k * ld, dH.data_ptr(),
+                              ld, m * ld, flags=P.LEAN)
+    torch.cuda.synchronize()
+    got, hand = dC.cpu().numpy(), dH.cpu().numpy()
+    assert mismatches(got[:, :, :n], hand[:, :, :n]) == 0
+    assert (got[:, :, n:] == 7.0).all()
+    ref = O.ref_gemm(A, B, k, n)
+    d = planes_diff(got, ref, W, n)
+    assert d <= 0.05 * 4 * k * U_P[W], d / (4 * k * U_P[W])
+    with pytest.raises(ValueError, match="MPFK_LEAN only"):
+        P.gemm_device_acc(W, m, n, 16, dA.data_ptr(), A.shape[2], m * A.shape[2], dBfull.data_ptr(), ld, k * ld,
+                          dH.data_ptr(), ld, m * ld, flags=P.FAST)
