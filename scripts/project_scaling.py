@@ -31,6 +31,9 @@ from paper_2101_06584_b200.dist import shard_rows  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="dd8192")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--lean", action="store_true",
+                help="flags = MPFK_LEAN (tolerance mode): the plain and staged legs only; each shard is compared "
+                     "with the one-shot lean product's rows (plain: bitwise; staged: within 4*k*u_p)")
 a = ap.parse_args()
 W, n, wide = WORKLOADS[a.workload]
 ld = P.pad_columns(n)
@@ -53,13 +56,43 @@ def timed(fn):
 
 
 ref = torch.zeros_like(A)
-P.gemm_device(W, n, n, n, A.data_ptr(), ld, n * ld, B.data_ptr(), ld, n * ld, ref.data_ptr(), ld, n * ld,
-              s.cuda_stream)
+P.gemm_device_ex(W, n, n, n, A.data_ptr(), ld, n * ld, B.data_ptr(), ld, n * ld, ref.data_ptr(), ld, n * ld,
+                 P.LEAN if a.lean else P.BIT_EXACT, s.cuda_stream)
+U_P = {2: 2.0 ** -104, 3: 2.0 ** -156, 4: 2.0 ** -208}
+
+
+def lean_leg(N, r0, r1, rows, Ash, slices, cuts, t1):
+    """plain and staged with MPFK_LEAN"""
+    Csh = torch.zeros((W, rows, ld), dtype=torch.float64, device="cuda")
+    plain = timed(lambda: P.gemm_device_ex(W, rows, n, n, Ash.data_ptr(), ld, rows * ld, B.data_ptr(), ld, n * ld,
+                                           Csh.data_ptr(), ld, rows * ld, P.LEAN, s.cuda_stream))
+    same = bool(torch.equal(Csh.view(torch.int64), ref[:, r0:r1].view(torch.int64)))  # shard-independent
+    Cs, Bst = torch.zeros_like(Csh), torch.zeros_like(B)
+    ts = timed(lambda: P.gemm_device_staged(W, rows, n, n, Ash.data_ptr(), ld, rows * ld, Bst.data_ptr(), ld, n * ld,
+                                            Cs.data_ptr(), ld, rows * ld, [x.data_ptr() for x in slices], cuts, 0,
+                                            s.cuda_stream, flags=P.LEAN))
+    d = Cs[W - 1] - ref[W - 1, r0:r1]
+    for w in range(W - 2, -1, -1):
+        d = d + (Cs[w] - ref[w, r0:r1])
+    diff = float(d[:, :n].abs().max() / ref[0, r0:r1, :n].abs().max()) / (4 * n * U_P[W])
+    t1 = plain if N == 1 else t1
+    print(json.dumps({"workload": a.workload, "flags": "MPFK_LEAN", "ranks": N, "rows_per_rank": rows,
+                      "plain_ms": round(plain, 3), "staged_ms": round(ts, 3), "plain_equals_one_shot_rows": same,
+                      "staged_diff_over_tolerance": round(diff, 6),
+                      "projected_efficiency_plain": round(t1 / (N * plain), 4),
+                      "projected_efficiency_staged": round(t1 / (N * ts), 4)}), flush=True)
+    return t1
+
+
 t1 = None
 for N in (1, 2, 4, 8):
     r0, r1 = shard_rows(n, N, 0)
     rows = r1 - r0
     Ash = A[:, r0:r1].contiguous()
+    if a.lean:
+        cuts = [shard_rows(n, N, r, 16)[0] for r in range(N)] + [n]
+        t1 = lean_leg(N, r0, r1, rows, Ash, [B[:, cuts[r]:cuts[r + 1]].contiguous() for r in range(N)], cuts, t1)
+        continue
     Csh = torch.zeros((W, rows, ld), dtype=torch.float64, device="cuda")
     plain = timed(lambda: P.gemm_device(W, rows, n, n, Ash.data_ptr(), ld, rows * ld, B.data_ptr(), ld, n * ld,
                                         Csh.data_ptr(), ld, rows * ld, s.cuda_stream))
