@@ -57,7 +57,7 @@ OPS_PER_MAC = {2: 20, 3: 132, 4: 218}
 # (m n k), profiles/r01b/metrics_*.csv): TD folds 11 operations on the
 # zero-extended fourth lane of td_add_q (DESIGN 4.1) and, in the fast pass,
 # skips the two operations of vseb's residual that only its rare path reads
-EXEC_OPS_PER_MAC = {2: 20, 3: 119, 4: 218}
+EXEC_OPS_PER_MAC = {2: 20, 3: 110, 4: 212}
 NAMES = {2: "DD", 3: "TD", 4: "QD"}
 L2_BYTES = 126 * 2 ** 20
 METRIC = "MPF Gflops (2mnk/s), DD/TD/QD GEMM"

@@ -56,6 +56,26 @@ MPFK_HD bool nz(double x) {
 #endif
 MPFK_HD double sel(bool p, double a, double b) { return p ? a : b; }
 
+// "a is at least in b's binade", conservatively: the high words with the
+// sign bit dropped compare like magnitudes, and equal high words mean equal
+// exponents.  On the device it is ONE instruction off the FP64 pipe: a
+// binary32 compare of the high words with |.| operand modifiers.  High words
+// that read as binary32 NaN (|x| >= 2^1017, infinities, NaNs) compare false:
+// conservative (the caller then takes the exact form).
+#if defined(__CUDA_ARCH__)
+MPFK_HD bool mag_ge(double a, double b) {
+  return fabsf(__int_as_float(__double2hiint(a))) >= fabsf(__int_as_float(__double2hiint(b)));
+}
+#else
+MPFK_HD bool mag_ge(double a, double b) {
+  uint64_t ua, ub;
+  std::memcpy(&ua, &a, sizeof ua);
+  std::memcpy(&ub, &b, sizeof ub);
+  const uint32_t ha = static_cast<uint32_t>(ua >> 32) & 0x7fffffffu, hb = static_cast<uint32_t>(ub >> 32) & 0x7fffffffu;
+  return ha <= 0x7f800000u && hb <= 0x7f800000u && ha >= hb;  // (binary32 NaN patterns are unordered)
+}
+#endif
+
 // "This input left the fast form" accumulators for the GEMM inner loop (the
 // `rare` argument of the *_t forms below): need_nz(x) records that x had to
 // be nonzero, any() reports whether some recorded x was zero.
@@ -67,6 +87,8 @@ struct RareBool {
   MPFK_HD void need_nz(double x) { r |= !nz(x); }
   MPFK_HD void need_nz(double x, double y) { r |= !(nz(x) & nz(y)); }
   MPFK_HD void need_nz(double x, double y, double z) { r |= !(nz(x) & nz(y) & nz(z)); }
+  // a had to be at least b's binade (two_sum_ordered below)
+  MPFK_HD void need_ge(double a, double b) { r |= !mag_ge(a, b); }
   MPFK_HD bool any() const { return r; }
 };
 // RareMin: a running minimum of |high word read as binary32| -- one FMNMX3
@@ -89,6 +111,7 @@ struct RareMin {
   MPFK_HD void need_nz(double x) { m = fminf(m, key(x)); }
   MPFK_HD void need_nz(double x, double y) { m = fminf(fminf(m, key(x)), key(y)); }
   MPFK_HD void need_nz(double x, double y, double z) { need_nz(x, y), need_nz(z); }
+  MPFK_HD void need_ge(double a, double b) { m = mag_ge(a, b) ? m : 0.0f; }
   MPFK_HD bool any() const { return m == 0.0f; }
 #else
   bool r = false;
@@ -100,6 +123,7 @@ struct RareMin {
   MPFK_HD void need_nz(double x) { r |= hz(x); }
   MPFK_HD void need_nz(double x, double y) { r |= hz(x) | hz(y); }
   MPFK_HD void need_nz(double x, double y, double z) { r |= hz(x) | hz(y) | hz(z); }
+  MPFK_HD void need_ge(double a, double b) { r |= !mag_ge(a, b); }
   MPFK_HD bool any() const { return r; }
 #endif
 };
@@ -157,6 +181,21 @@ MPFK_HD void two_sum_sorted(double a, double b, double& s, double& e) {
   s = ss;
 }
 
+// two_sum_sorted without the sort, for the GEMM's fast pass: where the
+// operands' order is known with overwhelming probability (a leading product
+// against the sum of its lower-order terms), take a as the larger one --
+// 3 FP64 operations, the same bits as Knuth's form whenever exponent(a) >=
+// exponent(b) (see above) -- and tell `rare` when that did not hold, so the
+// caller recomputes exactly.  The test is one compare instruction off the
+// FP64 pipe (mag_ge).
+template <class Rare>
+MPFK_HD void two_sum_ordered(double a, double b, double& s, double& e, Rare& rare) {
+  rare.need_ge(a, b);
+  const double ss = add(a, b);
+  e = add(sub(a, ss), b);
+  s = ss;
+}
+
 #ifdef MPFK_TWO_SUM_SORTED
 MPFK_HD void two_sum(double a, double b, double& s, double& e) { two_sum_sorted(a, b, s, e); }
 #else
@@ -183,6 +222,21 @@ MPFK_HD void three_sum(double a, double b, double c, double& s, double& e1, doub
   double ts, te, us, ue;
   two_sum(a, b, ts, te);
   two_sum(c, ts, us, ue);
+  two_sum(te, ue, e1, e2);
+  s = us;
+}
+
+// three-sum for the GEMM's fast pass when c is the rounding error of a sum
+// that feeds a or b (so a + b is all but never below c's binade): the middle
+// two-sum takes the ordered 3-operation form, larger operand first --
+// two_sum(c, ts) and two_sum(ts, c) are the same bits (same rounded sum, same
+// exact error, +0 when it vanishes) -- and `rare` hears when the order did
+// not hold.
+template <class Rare>
+MPFK_HD void three_sum_c_small(double a, double b, double c, double& s, double& e1, double& e2, Rare& rare) {
+  double ts, te, us, ue;
+  two_sum(a, b, ts, te);
+  two_sum_ordered(ts, c, us, ue, rare);
   two_sum(te, ue, e1, e2);
   s = us;
 }
@@ -383,10 +437,17 @@ MPFK_HD void qd_mul_t(const double* x, const double* y, double* r, Rare& rare) {
   three_sum(p1, p2, q0, p1, p2, q0);
   double gs, ge;
   two_sum(q1, q2, gs, ge);
-  three_sum(p2, gs, ge, p2, q1, q2);
   double hs, he;
   two_sum(p3, p5, hs, he);
-  three_sum(hs, p4, he, p3, p4, p5);
+  if (kFast) {
+    // ge and he are the rounding errors of gs and hs: below p2 + gs and
+    // hs + p4 unless those cancel to within an ulp
+    three_sum_c_small(p2, gs, ge, p2, q1, q2, rare);
+    three_sum_c_small(hs, p4, he, p3, p4, p5, rare);
+  } else {
+    three_sum(p2, gs, ge, p2, q1, q2);
+    three_sum(hs, p4, he, p3, p4, p5);
+  }
 
   double s0, t0, s1, t1;
   two_sum(p2, p3, s0, t0);
@@ -429,12 +490,18 @@ MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, Rare& rare)
   two_sum(x[2], y[2], s2, t2);
   two_sum(s1, t0, s1, t0);
   three_sum(s2, t0, t1, s2, t0, t1);
-  // three_sum2(+0, t0, t2), eft.hpp:95-99, with the folds above
-  const double ts = add(0.0, t0);
+  // three_sum2(+0, t0, t2), eft.hpp:95-99, with the folds above.  The three
+  // additions of +0 the folds leave (+0 + t0, +0 + u.e, (..) + t3) only map
+  // -0 to +0, and none of their operands can be -0: a Knuth two-sum error is
+  // never -0 (its last add is -0 only if both addends are, i.e. b = -0 with
+  // v = s - a = +0, and then a - (s - v) = +0), so neither is a sum of two
+  // such errors (t0 here is three_sum's e1 = te + ue; -0 needs both -0).
+  // They are identities and are not executed: 116 operations per
+  // multiply-add (tests/test_arith_host.py sweeps signed zeros against the
+  // reference build).
   double s3, ue;
-  two_sum(t2, ts, s3, ue);
-  t0 = add(0.0, ue);
-  t0 = add(add(t0, t1), 0.0);
+  two_sum(t2, t0, s3, ue);
+  t0 = add(ue, t1);
   double r3;
   renorm5_t<kFast, true>(s0, s1, s2, s3, t0, r[0], r[1], r[2], r3, rare);
 }
@@ -471,8 +538,15 @@ MPFK_HD void td_mul_t(const double* x, const double* y, double* r, Rare& rare) {
   // vec_sum<4>(z00.s, b0, b1, s3)
   double e0, e1, e2, e3;
   two_sum(b1, s3, s, e3);
-  two_sum(b0, s, s, e2);
-  two_sum(z00s, s, e0, e1);
+  if (kFast) {
+    // b0 leads the order-1 terms and z00.s is the leading product: each is
+    // (all but never) at least in the binade of the sum of what lies below it
+    two_sum_ordered(b0, s, s, e2, rare);
+    two_sum_ordered(z00s, s, e0, e1, rare);
+  } else {
+    two_sum(b0, s, s, e2);
+    two_sum(z00s, s, e0, e1);
+  }
   r[0] = e0;
   if (kFast) {
     double a, rr, b, r2;
