@@ -658,7 +658,7 @@ U_P = {2: 2.0 ** -104, 3: 2.0 ** -156, 4: 2.0 ** -208}  # north star
 def measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream, slices=None):
     """The same device-resident GEMM with flags = MPFK_LEAN (the north star's
     tolerance mode: 10 / 42 / 107 FP64 instructions per multiply-add instead
-    of 20 / 119 / 218; NOT bit-identical to the reference).  Timed like the
+    of the bit-exact kernels' 20 / 110 / 212; NOT bit-identical to the reference).  Timed like the
     bit-exact steps (N > 1: the staged all-gather -> GEMM of every rank's
     shard, max over ranks); its result is compared with theirs (dC,
     bit-identical to the reference) as a normwise difference in units of

@@ -478,9 +478,10 @@ MPFK_HD void qd_mul(const double* x, const double* y, double* r) {
 //      e = (+0 - +0) + (b - s) = +0 + (b - s), where b - s is +0 for b != -0
 //      and -0 - +0 = -0 for b = -0; +0 + (+-0) = +0.  Hence (s, e) =
 //      (+0 + b, +0): one add instead of six.
-//  * three_sum2's error t.e + u.e = +0 + u.e stays one add (it maps -0 to +0).
-//  * t0 + t3 with t3 = +0 stays (same reason).
-// 11 of td_add_q's 85 FP64 operations disappear; results are unchanged
+//  * three_sum2's error t.e + u.e = +0 + u.e, the +0 + t0 in front of it and
+//    t0 + t3 with t3 = +0 only map -0 to +0, and their operands are never -0
+//    (see the function body): identities too.
+// 14 of td_add_q's 85 FP64 operations disappear; results are unchanged
 // (tests/test_arith_host.py sweeps signed zeros against the reference).
 template <int kFast, class Rare = RareBool>
 MPFK_HD void td_add_q_t(const double* x, const double* y, double* r, Rare& rare) {

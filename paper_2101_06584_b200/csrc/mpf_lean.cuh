@@ -1,6 +1,6 @@
 // mpf_lean.cuh -- the MPFK_LEAN multiply-accumulate: C += a*b for DD/TD/QD
 // with 10 / 42 / 107 FP64 operations instead of the reference sequence's
-// 20 / 119 (132 counted) / 218.
+// 20 / 110 (132 counted) / 212 (218 counted).
 //
 // NOT the reference's arithmetic and NOT bit-identical to it: this is the
 // north star's tolerance mode (BASELINE.json: "each component of C must
