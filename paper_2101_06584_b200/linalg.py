@@ -198,7 +198,7 @@ def gemm_into(C_: MPMatrix, A: MPMatrix, B: MPMatrix, n_gpus: int = 1, flags: in
     matmul_block_parallel_into; flags=FAST may split K for outputs too small
     to fill the GPU (deterministic, tolerance-checked: normwise 4*k*u_p);
     flags=LEAN runs the tolerance-mode arithmetic (csrc/mpf_lean.cuh: 12 / 46 /
-    113 FP64 instructions per multiply-add, 1.75-2.75x the bit-exact rate, NOT
+    113 FP64 instructions per multiply-add, 1.75-2.6x the bit-exact rate, NOT
     the reference's bits).  FAST | LEAN combines them."""
     W = _check_same_width(C_, A, B)
     c, a, b = C_._c(), A._c(), B._c()
