@@ -150,7 +150,7 @@ int mpfk_last_stats(mpfk_stats *out);
  *   element as W overlapping levels fed by exact two-sum cascades, pulls them
  *   back once per 16 k steps and normalises once at the end
  *   (csrc/mpf_lean.cuh: 10 / 42 / 107 FP64 instructions per multiply-add, 1.75x /
- *   2.75x / 2.0x the bit-exact GEMM's rate on a B200).  NOT bit-identical to
+ *   2.6x / 1.96x the bit-exact GEMM's rate on a B200).  NOT bit-identical to
  *   the reference; results are canonical normalised values within the same
  *   normwise 4*k*u_p (measured: 1e-4..4e-3 of it on the BASELINE inputs,
  *   i.e. less accurate than the reference's own 4e-6..2e-4), deterministic
