@@ -174,7 +174,13 @@ MPFK_HD uint32_t mag_key(double x) {
 // stays bit-identical (tests/test_arith_host.py checks it against Knuth's
 // form on signed zeros, subnormals, ties and cancelling pairs).
 MPFK_HD void two_sum_sorted(double a, double b, double& s, double& e) {
+#if defined(MPFK_TWO_SUM_SORTED_FSETP)
+  // experiment: the order from ONE binary32 compare of the high words
+  // (mag_ge); NOT exact for |x| >= 2^1017, whose high words read as NaN
+  const bool p = mag_ge(a, b);
+#else
   const bool p = mag_key(a) >= mag_key(b);
+#endif
   const double x = sel(p, a, b), y = sel(p, b, a);
   const double ss = add(a, b);
   e = add(sub(x, ss), y);
