@@ -50,6 +50,15 @@ out["fast_deterministic"] = P.bits_equal(F1, F2)
 E = P.matmul_block(A, B)
 d = np.abs(F1.data[0] - E.data[0]).max()
 out["fast_close"] = bool(d <= 4 * 4000 * 2.0 ** -156 * np.abs(E.data[0]).max() + 1e-300)
+# LEAN across devices: every element is the same chain whatever the row
+# shard, so G devices give the one-device lean result bit for bit
+A = P.fill_baseline(4, 390, 500, 7, wide=True)
+B = P.fill_baseline(4, 500, 130, 8, wide=True)
+L1 = P.gemm(A, B, n_gpus=1, flags=P.LEAN)
+LG = P.gemm(A, B, n_gpus=0, flags=P.LEAN)
+out["lean_devices"] = P.last_stats()["n_gpus"]
+out["lean_same_on_all_devices"] = P.bits_equal(L1, LG)
+out["lean_is_not_the_reference_bits"] = not P.bits_equal(L1, P.matmul_block(A, B))
 print(json.dumps(out))
 """
 
@@ -72,3 +81,5 @@ def test_multi_device_host_path_emulated(gpu_lib, emulated):
     assert out["gemm_all_devices"] == emulated
     assert out["gemm_same"]
     assert out["fast_deterministic"] and out["fast_close"]
+    assert out["lean_devices"] == emulated and out["lean_same_on_all_devices"]
+    assert out["lean_is_not_the_reference_bits"]
