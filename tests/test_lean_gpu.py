@@ -261,3 +261,23 @@ def test_lean_k_panels_and_staged_gather(gpu_lib, W):
     with pytest.raises(ValueError, match="MPFK_LEAN only"):
         P.gemm_device_acc(W, m, n, 16, dA.data_ptr(), A.shape[2], m * A.shape[2], dBfull.data_ptr(), ld, k * ld,
                           dH.data_ptr(), ld, m * ld, flags=P.FAST)
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+def test_lean_edge_shapes_exact_small_values(gpu_lib, W):
+    """empty and one-element shapes through the host API; products of small
+    exactly representable values are exact in both modes, so they agree
+    bitwise, pads +0"""
+    P = gpu_lib
+    for (m, k, n) in [(0, 5, 3), (4, 0, 3), (4, 5, 0), (1, 1, 1), (33, 1, 2), (2, 17, 1)]:
+        A, B = P.MPMatrix(W, m, k), P.MPMatrix(W, k, n)
+        if m and k:
+            A.data[0, :, :k] = 1.5
+        if k and n:
+            B.data[0, :, :n] = -2.0
+        Cm = P.gemm(A, B, flags=P.LEAN)
+        E = P.matmul_block(A, B)
+        assert Cm.data.shape == E.data.shape
+        if m and n:
+            assert np.array_equal(Cm.data, E.data), (W, m, k, n)
+            assert not np.signbit(Cm.data[:, :, n:]).any()
