@@ -137,7 +137,7 @@ struct TileCfg {
   static constexpr bool VSEBF = FASTR && VSEBF_;          // td_mul's vseb common case in the fast pass
   // the fast pass's "left the fast form" accumulator: exact LOP3/PLOP3
   // predicates (arith::RareBool, the product) or a running FMNMX3 minimum
-  // (arith::RareMin: 14 of TD's 48 and 83 of QD's 205 non-FP64 instructions
+  // (arith::RareMin, measured before the ordered two-sums: 14 of TD's 48 and 83 of QD's 205 non-FP64 instructions
   // per loop body fewer, yet 0.3-0.7 % SLOWER on the B200,
   // profiles/r02/tune_raremin.log -- kept as a measured alternative)
   using Rare = typename std::conditional<RAREMIN_ != 0, arith::RareMin, arith::RareBool>::type;
