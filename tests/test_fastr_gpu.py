@@ -77,3 +77,27 @@ def test_random_inputs_bitwise_and_redo_rate(gpu_lib, W):
     warp_ktiles = (m * n // 32) * ((k + 15) // 16)
     assert redo <= warp_ktiles // 100, (redo, warp_ktiles)
     assert mismatches(got[:, :, :n], O.ref_gemm(A, B, k, n)[:, :, :n]) == 0
+
+
+@pytest.mark.parametrize("W", (3, 4))
+@pytest.mark.parametrize("which", ("A", "B", "both"))
+def test_redo_when_two_sum_order_fails(gpu_lib, W, which):
+    """The fast pass's ordered two-sums (two_sum_ordered, three_sum_c_small)
+    assume a leading product at least in the binade of its lower-order
+    terms.  Operands whose components are NOT in decreasing order (here:
+    reversed, every value nonzero so no zero-residual path is involved) break
+    that; the warps must notice (mag_ge), recompute exactly, and the result
+    stays bit-identical to the reference, which accepts any operands."""
+    P = gpu_lib
+    m, k, n = 64, 96, 64
+    A = random_signed(W, m, k, 9700 + W)
+    B = random_signed(W, k, n, 9800 + W)
+    if which in ("A", "both"):
+        A = np.ascontiguousarray(A[::-1])
+    if which in ("B", "both"):
+        B = np.ascontiguousarray(B[::-1])
+    P.gemm_redo_count(reset=True)
+    got = device_gemm(P, A, B, m, k, n)
+    redo = P.gemm_redo_count(reset=True)
+    assert redo > 0, "reversed components should fail the order test"
+    assert mismatches(got[:, :, :n], O.ref_gemm(A, B, k, n)[:, :, :n]) == 0
