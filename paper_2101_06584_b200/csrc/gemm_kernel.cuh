@@ -102,8 +102,11 @@ __device__ __forceinline__ void cp_async16_full(unsigned smem_addr, const void* 
 // tile row.
 template <int W_, int BM_, int BN_, int BK_, int TM_, int TN_, int STAGES_ = 2, int KUNROLL_ = 1,
           int GROUP_M_ = 16, int MINB_ = 1, int FIXK_ = 0, int ONEBAR_ = 0, int FASTR_ = 0, int VSEBF_ = 0,
-          int FLOAD_ = 1, int PAIRB_ = 1, int RAREMIN_ = 0, int LEAN_ = 0>
+          int FLOAD_ = 1, int PAIRB_ = 1, int RAREMIN_ = 0, int LEAN_ = 0, int ROWMAJ_ = 0>
 struct TileCfg {
+  // bit-exact DD: a micro-tile row's multiply-adds written stage by stage
+  // (arith::dd_mac_row: the same operations in another order)
+  static constexpr int ROWMAJ = (W_ == 2 && !LEAN_) ? ROWMAJ_ : 0;
   // MPFK_LEAN (mpf_lean.cuh): the tolerance-mode multiply-accumulate --
   // every element is W levels fed by exact two-sum cascades, pulled back to
   // nearly non-overlapping once per k-tile and normalised once at the end.
@@ -420,14 +423,19 @@ __device__ __forceinline__ void mac_step(double (&acc)[Cfg::TM][Cfg::TN][Cfg::W]
 #pragma unroll
     for (int w = 0; w < W; ++w) a[i][w] = As[w * BM * Cfg::AS + (ty + i * TY) * Cfg::AS + kk];
   load_b<Cfg>(b, Bs, tx, kk);
+  if constexpr (Cfg::ROWMAJ) {
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < TM; ++i) arith::dd_mac_row<TN>(acc[i], a[i], b);
+  } else {
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      double p[W];
-      arith::mp_mul<W>(a[i], b[j], p);
-      arith::mp_add<W>(acc[i][j], p, acc[i][j]);
-    }
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        double p[W];
+        arith::mp_mul<W>(a[i], b[j], p);
+        arith::mp_add<W>(acc[i][j], p, acc[i][j]);
+      }
+  }
 }
 
 // mac_step with the branch-free renormalisation (Cfg::FASTR); ORs into

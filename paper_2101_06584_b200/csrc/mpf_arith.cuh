@@ -404,6 +404,51 @@ MPFK_HD void dd_mul(const double* x, const double* y, double* r) {
   qts(p, e, r[0], r[1]);
 }
 
+// N DD multiply-adds acc[j] = dd_add(acc[j], dd_mul(a, b[j])) that share a
+// (one row of a thread's micro-tile), written stage by stage across the N
+// elements: the operations and their operands are exactly those of dd_mul
+// followed by dd_add, element by element -- bit-identical -- only the order
+// in the instruction stream differs (consecutive instructions independent,
+// the shared operand a in the same slot).
+template <int N>
+MPFK_HD void dd_mac_row(double (&acc)[N][2], const double* a, const double (&b)[N][2]) {
+  double p[N], e[N], t[N], r0[N], s[N], v[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) p[j] = mul(a[0], b[j][0]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) t[j] = mul(a[0], b[j][1]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = mul(a[1], b[j][0]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = fma(a[0], b[j][0], -p[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) t[j] = add(t[j], v[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = add(e[j], t[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) r0[j] = add(p[j], e[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) s[j] = add(acc[j][0], r0[j]);      // two_sum(acc0, r0): the sum
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = sub(e[j], sub(r0[j], p[j]));  // r1 of qts(p, e)
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = sub(s[j], acc[j][0]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) t[j] = sub(s[j], v[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = add(acc[j][1], e[j]);         // w = x1 + y1
+#pragma unroll
+  for (int j = 0; j < N; ++j) t[j] = add(sub(acc[j][0], t[j]), sub(r0[j], v[j]));  // two_sum error
+#pragma unroll
+  for (int j = 0; j < N; ++j) e[j] = add(t[j], e[j]);
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const double hi = add(s[j], e[j]);
+    acc[j][1] = sub(e[j], sub(hi, s[j]));
+    acc[j][0] = hi;
+  }
+}
+
 // qd_add, mpf.hpp:178-196 (63 ops + renorm5).  With Trunc3 the fourth
 // output is not produced (td_add_q drops it, mpf.hpp:141), which lets the
 // compiler delete the dead tail of renorm5.
