@@ -69,6 +69,21 @@ def test_guard_gemm_device_acc_fast(gpu_lib, W, m, n, k):
     if P.splitk_segments(W, m, n, k) == 1:
         assert mismatches(got3, want[:, :, :n]) == 0
     assert outside_untouched(bC3, m, n)
+    # LEAN (tolerance mode): the same windows -- a margin read would put a NaN
+    # into the result, a stray write would change a sentinel; every cell is
+    # the host chain of the same source (tests/csrc/arith_host.cpp)
+    import ctypes as C
+    import os
+    H = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libarith_host.so"))
+    H.hst_lean_gemm.argtypes = [C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_size_t, C.c_void_p,
+                                C.c_size_t, C.c_void_p, C.c_size_t]
+    chain = np.zeros((W, m, n))
+    assert H.hst_lean_gemm(W, m, k, n, A.ctypes.data, A.shape[2], B.ctypes.data, B.shape[2], chain.ctypes.data, n) == 0
+    bC4, pC4, _, _ = window(P, torch, W, m, n, SENT)
+    P.gemm_device_ex(W, m, n, k, pA, lda, pa, pB, ldb, pb, pC4, ldc, pc, P.LEAN)
+    torch.cuda.synchronize()
+    assert mismatches(bC4.cpu().numpy()[:, 3:3 + m, 4:4 + n], chain) == 0
+    assert outside_untouched(bC4, m, n)
 
 
 @pytest.mark.parametrize("W,m,n,k", CASES[:3])
