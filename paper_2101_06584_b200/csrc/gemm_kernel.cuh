@@ -143,7 +143,10 @@ struct TileCfg {
   // (arith::RareMin, measured before the ordered two-sums: 14 of TD's 48 and 83 of QD's 205 non-FP64 instructions
   // per loop body fewer, yet 0.3-0.7 % SLOWER on the B200,
   // profiles/r02/tune_raremin.log -- kept as a measured alternative)
-  using Rare = typename std::conditional<RAREMIN_ != 0, arith::RareMin, arith::RareBool>::type;
+  // (RAREMIN_ = 2: arith::RareHi, every test one binary32 compare of the high words)
+  using Rare = typename std::conditional<
+      RAREMIN_ == 1, arith::RareMin,
+      typename std::conditional<RAREMIN_ == 2, arith::RareHi, arith::RareBool>::type>::type;
   static constexpr int SNAP = FASTR ? THREADS * TM * TN * W : 0;  // doubles
   static_assert(!FASTR || THREADS % 32 == 0, "the warp-level redo votes over full warps");
   static constexpr int APAD = 2, BPAD = 2;  // keep 16 B row alignment, spread banks
