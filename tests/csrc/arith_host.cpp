@@ -214,6 +214,17 @@ void hst_two_sum_pair_batch(std::size_t count, const double* a, const double* b,
   }
 }
 
+// two_sum_ordered (the fast pass's 3-operation form) next to Knuth's form:
+// out = (s_knuth, e_knuth, s_ordered, e_ordered), flag = the order test failed
+void hst_two_sum_ordered_batch(std::size_t count, const double* a, const double* b, double* out, int* flag) {
+  for (std::size_t i = 0; i < count; ++i) {
+    RareBool rare;
+    two_sum_knuth(a[i], b[i], out[4 * i], out[4 * i + 1]);
+    two_sum_ordered(a[i], b[i], out[4 * i + 2], out[4 * i + 3], rare);
+    flag[i] = rare.any();
+  }
+}
+
 int hst_fast_mac_batch(int W, int level, std::size_t count, const double* a, const double* b,
                        const double* acc, double* out, int* flags) {
   for (std::size_t i = 0; i < count; ++i) {

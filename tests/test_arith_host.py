@@ -263,3 +263,36 @@ def test_fast_forms_flag_every_departure(H, W, level):
     assert not bad.any(), (a[bad][:3], b[bad][:3], acc[bad][:3])
     assert not ((flags[:, 0] == 1) & (flags[:, 1] == 0)).any(), "RareMin missed a departure"
     assert clear.sum() > 5000 and (~clear).sum() > 100  # both sides exercised
+
+
+def test_two_sum_ordered_equals_knuth_when_the_order_holds(H):
+    """The fast pass's ordered two-sum (3 operations, first operand assumed
+    at least in the second's binade): identical bits to Knuth's form whenever
+    its order test (mag_ge: one compare of the high words) did not flag --
+    including signed zeros, ties, subnormals and cancelling pairs -- and the
+    test flags every pair whose exponents are the other way round."""
+    H.hst_two_sum_ordered_batch.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(77)
+    n = 400000
+    a = rng.standard_normal(n) * np.ldexp(1.0, rng.integers(-40, 41, size=n))
+    b = rng.standard_normal(n) * np.ldexp(1.0, rng.integers(-40, 41, size=n))
+    special = np.array([0.0, -0.0, 1.0, -1.0, 2.0 ** -1074, -2.0 ** -1074, 2.0 ** -1060, 1.0 + 2.0 ** -52,
+                        2.0 ** 52, 2.0 ** 53 + 2.0, 0.5, -0.5, 3.0, 2.0 ** -1022, 2.0 ** 1000, -2.0 ** 1000])
+    a[:65536] = np.repeat(special, 4096)[:65536]
+    b[:65536] = np.tile(np.repeat(special, 256), 16)[:65536]
+    a[65536:70000] = -b[65536:70000]                      # exact cancellation
+    a[70000:80000] = b[70000:80000] * (1 + 2.0 ** -30)    # near ties
+    out = np.zeros((n, 4))
+    flag = np.zeros(n, dtype=np.int32)
+    H.hst_two_sum_ordered_batch(n, a.ctypes.data, b.ctypes.data, out.ctypes.data, flag.ctypes.data)
+    clear = flag == 0
+    k, o = out[:, :2].view(np.uint64), out[:, 2:].view(np.uint64)
+    bad = (k != o).any(axis=1) & clear
+    assert not bad.any(), (a[bad][:5], b[bad][:5])
+    # the sum is the same rounded sum either way
+    assert np.array_equal(k[:, 0], o[:, 0])
+    # every pair with exponent(a) < exponent(b) is flagged (finite values)
+    ea, eb = np.frexp(a)[1], np.frexp(b)[1]
+    must = (ea < eb) & (b != 0) & (np.abs(a) >= 2.0 ** -1022) & (np.abs(b) >= 2.0 ** -1022)
+    assert flag[must].all()
+    assert clear.sum() > 100000 and (~clear).sum() > 100000
