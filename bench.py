@@ -86,6 +86,9 @@ def parse(argv=None):
     ap.add_argument("--cpu-steps", type=int, default=3, help="cpu_baseline: timed reference calls (median)")
     ap.add_argument("--no-lean", action="store_true",
                     help="skip the MPFK_LEAN (tolerance mode) leg reported next to each bit-exact workload")
+    ap.add_argument("--lean-dist", action="store_true",
+                    help="N > 1: also run the MPFK_LEAN leg over the staged transport (off by default: the "
+                         "multi-rank line is about the bit-exact headline; always on with --emulate-on-one-gpu)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--transport", choices=TRANSPORTS, default=None,
                     help="N > 1 replication of B: staged (copy engines gather B's growing K panels from the "
@@ -535,7 +538,7 @@ def measure_workload(ctx, workload, steps, warmup, with_cpu):
 
     lean = None
     if not args.no_lean and ((ws == 1 and rows and slices is None and transport not in ("nccl", "bcast")) or
-                             (slices is not None and transport == "staged")):
+                             (slices is not None and transport == "staged" and (args.lean_dist or ctx.emulate))):
         lean = measure_lean(ctx, W, dA, dB, dC, rows, n, k, ld, steps, flush, stream, slices=slices)
 
     step_ms = [a.elapsed_time(c) for a, _, c in evs]

@@ -48,7 +48,7 @@ def test_torchrun_fused_allgather_path(gpu_lib, mode, launches):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--workload", "td1024",
            "--steps", "2", "--warmup", "1", "--no-e2e", "--no-cpu-baseline", "--dist",
-           "--transport", mode, "--pull-panel", "64", "--pull-chunk", "8", "--extra", "none"]
+           "--transport", mode, "--pull-panel", "64", "--pull-chunk", "8", "--extra", "none", "--lean-dist"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
